@@ -1,0 +1,230 @@
+/* hetplan_b200.h — C ABI of the B200-native candidate-evaluation engine.
+ *
+ * Drop-in boundary for the reference planner's hot path:
+ *   SearchOutcome hetplan::search(const ModelSpec&, const ClusterSpec&,
+ *                                 const TrainConfig&, const PlannerConfig&, int jobs)
+ *   (/root/reference/proj/core/include/hetplan/planner.hpp:115-116,
+ *    implementation planner.cpp:579-685).
+ * The reference exposes no FFI; this header is the flat, exception-free
+ * equivalent (plain structs, pointers and sizes, no C++/torch types). The C++
+ * mirror with the reference's exact signature lives in hetplan_b200.hpp and is
+ * implemented over these entry points.
+ *
+ * Every entry point returns an hp_status; on failure hp_last_error(ctx) holds a
+ * message. Status codes follow the reference's exception kinds
+ * (errors.hpp:26-44, mapped to CLI exit codes at tools/cli.cpp:193-212):
+ *   HP_BAD_CONFIG  <- ConfigError        (exit 1)
+ *   HP_INFEASIBLE  <- InfeasibleError    (exit 2)
+ *   HP_CUDA/HP_NCCL/HP_INTERNAL <- anything else (exit 3)
+ */
+#ifndef HETPLAN_B200_H_
+#define HETPLAN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HP_ABI_VERSION 1
+#define HP_MAX_GROUPS 8      /* device groups (accelerator types) per cluster */
+#define HP_MAX_STAGES 256    /* pipeline stages per plan */
+#define HP_NAME_LEN 32
+
+typedef enum hp_status {
+  HP_OK = 0,
+  HP_BAD_CONFIG = 1,
+  HP_INFEASIBLE = 2,
+  HP_CUDA = 3,
+  HP_NCCL = 4,
+  HP_INTERNAL = 5,
+} hp_status;
+
+typedef enum hp_schedule { HP_GPIPE = 0, HP_1F1B = 1 } hp_schedule;         /* types.hpp:134 */
+typedef enum hp_scope { HP_INTRA_NODE = 0, HP_INTER_NODE = 1, HP_INTER_GROUP = 2 } hp_scope; /* types.hpp:63 */
+typedef enum hp_path { HP_GPU_DIRECT = 0, HP_CPU_STAGED = 1 } hp_path;       /* types.hpp:75 */
+
+/* ModelSpec, types.hpp:28-44 */
+typedef struct hp_model {
+  int32_t num_layers;
+  int32_t num_heads;
+  int64_t hidden_size;
+  int64_t seq_length;
+  int64_t vocab_size;
+  int32_t bytes_per_element;
+  int32_t _pad0;
+  double activation_bytes_per_token_per_hidden;
+  double edge_layer_cost_multiplier;
+} hp_model;
+
+/* DeviceGroup, types.hpp:47-61 */
+typedef struct hp_group {
+  char name[HP_NAME_LEN];
+  double peak_tflops;
+  double memory_bytes;
+  int32_t node_count;
+  int32_t devices_per_node;
+  double compute_efficiency;
+  double bwd_fwd_ratio;
+} hp_group;
+
+/* Link + LinkScope, types.hpp:67-88; groups referenced by index into
+ * hp_cluster.groups (the reference stores names and resolves them by linear
+ * scan, types.cpp:26-56). group_b is ignored unless scope == HP_INTER_GROUP. */
+typedef struct hp_link {
+  int32_t scope;
+  int32_t path;
+  int32_t group_a;
+  int32_t group_b;
+  double bandwidth_bits_per_s;
+  double latency_s;
+  double efficiency;
+  double staging_copy_bytes_per_s;
+} hp_link;
+
+/* ClusterSpec, types.hpp:90-103 */
+typedef struct hp_cluster {
+  int32_t n_groups;
+  int32_t n_links;
+  const hp_group* groups;
+  const hp_link* links;
+} hp_cluster;
+
+/* TrainConfig, types.hpp:105-113 */
+typedef struct hp_train {
+  int64_t global_batch_size;
+  int64_t micro_batch_size;
+  double optimizer_state_multiplier;
+} hp_train;
+
+/* PlannerConfig, planner.hpp:27-49. Empty lists take the reference defaults
+ * (planner.cpp:586-595). */
+typedef struct hp_planner {
+  int32_t n_pipeline_degrees;
+  int32_t n_micro_batch_candidates;
+  const int32_t* pipeline_degrees;
+  const int64_t* micro_batch_candidates;
+  double memory_headroom;
+  int64_t exhaustive_split_limit;
+  int32_t stage_order_beam_width;
+  int32_t uniform_split_only;
+  int32_t allow_group_interleaving;
+  int32_t time_bound_pruning;
+  int32_t schedule; /* hp_schedule */
+  int32_t _pad0;
+} hp_planner;
+
+typedef struct hp_problem {
+  hp_model model;
+  hp_cluster cluster;
+  hp_train train;
+  hp_planner planner;
+} hp_problem;
+
+/* StageAssignment, types.hpp:124-132 (group by index). */
+typedef struct hp_stage {
+  int32_t layer_begin;
+  int32_t layer_end;
+  int32_t group;
+  int32_t nodes_used;
+  int32_t tp_degree;
+  int32_t dp_degree;
+} hp_stage;
+
+/* ParallelPlan, types.hpp:136-154 (input digests are host-side provenance). */
+typedef struct hp_plan {
+  int32_t n_stages;
+  int32_t schedule;
+  int64_t micro_batches_per_dp_replica;
+  int64_t micro_batch_size;
+  hp_stage stages[HP_MAX_STAGES];
+} hp_plan;
+
+/* Search options. The candidate space is the reference's task list
+ * (planner.cpp:238-304) expanded into leaves (task, dp, B, tp vector;
+ * planner.cpp:353-391). A shard evaluates leaves whose position in that list
+ * satisfies the shard's partition (weighted, deterministic), so N shards
+ * together evaluate exactly the reference's candidates.
+ *
+ * Default mode (time_bound_pruning) needs the global probe bound
+ * (planner.cpp:640-651): a single-device search computes it itself; a
+ * sharded search passes the min over shards of hp_probe() in global_bound
+ * with have_global_bound = 1. */
+typedef struct hp_search_opts {
+  int32_t shard_index;
+  int32_t shard_count;
+  int32_t have_global_bound;
+  int32_t flags;       /* reserved, 0 */
+  double global_bound; /* used when have_global_bound */
+} hp_search_opts;
+
+/* Per-shard result. has_best = 0 when the shard simulated no candidate.
+ * best_time_s is the winner's iteration time (evaluate.cpp:90-97) with the
+ * exact bit pattern of the reference. Counts follow planner.cpp:425-432,513-515,
+ * 529-531,546 (memo hits are not counted; probe simulations are not counted).
+ * reason_counts tallies pruned candidates per reason (hp_reason). */
+typedef enum hp_reason {
+  HP_REASON_MEMORY = 0,       /* "stage i memory ... exceeds ..."        planner.cpp:509-515 */
+  HP_REASON_BOUND = 1,        /* "compute lower bound above incumbent"    planner.cpp:529-531 */
+  HP_REASON_NO_LINK = 2,      /* "no heterogeneous link between ..."      planner.cpp:317-327 */
+  HP_REASON_NO_ASSIGNMENT = 3,/* "no integral dp/tp/micro-batch assignment" planner.cpp:395-400 */
+  HP_REASON_COUNT = 4
+} hp_reason;
+
+typedef struct hp_result {
+  int64_t candidates_simulated;
+  int64_t candidates_pruned;
+  int64_t reason_counts[HP_REASON_COUNT];
+  int64_t leaves;          /* leaves this shard evaluated */
+  int64_t tasks;           /* tasks in the whole space */
+  int32_t has_best;
+  int32_t best_pp;
+  double best_time_s;
+  double global_bound;     /* probe bound used (inf when pruning is off) */
+  double device_ms;        /* kernel time of this call, CUDA events */
+  int64_t gpu_launches;    /* kernels this call launched */
+  hp_plan best_plan;
+} hp_result;
+
+typedef struct hp_ctx hp_ctx;
+
+/* Creates a context bound to CUDA device `device` (one context per GPU; a
+ * process may hold several). */
+hp_status hp_create(hp_ctx** out, int device);
+void hp_destroy(hp_ctx* ctx);
+const char* hp_last_error(const hp_ctx* ctx);
+int hp_abi_version(void);
+
+/* Validation of the specs (types.cpp:78-163) and planner config
+ * (planner.cpp:600-607). Host only. */
+hp_status hp_validate(hp_ctx* ctx, const hp_problem* problem);
+
+/* Probe pass for this shard (planner.cpp:640-651): min over the shard's tasks
+ * of the first simulated seed candidate. *bound = +inf when none. */
+hp_status hp_probe(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts* opts,
+                   double* bound);
+
+/* The hot path: enumerate, score and reduce this shard's candidates on the
+ * GPU. HP_INFEASIBLE is NOT returned for an empty shard (has_best = 0); the
+ * caller decides infeasibility after reducing over shards. */
+hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts* opts,
+                    hp_result* result);
+
+/* Argmin order of the reference (planner.cpp:178-200): returns <0 when
+ * (time_a, plan_a) ranks before (time_b, plan_b), >0 after, 0 if identical.
+ * Host only; used to reduce per-shard results. */
+int hp_better_than(const hp_problem* problem, double time_a, const hp_plan* plan_a,
+                   double time_b, const hp_plan* plan_b);
+
+/* Batched explicit-plan evaluation on the GPU: iteration_time_s of
+ * evaluate_plan_unchecked (evaluate.cpp:78-107) for n plans. Plans must be
+ * structurally valid (validate_plan, types.cpp:171-272). */
+hp_status hp_evaluate_plans(hp_ctx* ctx, const hp_problem* problem, const hp_plan* plans,
+                            int32_t n, double* iteration_time_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HETPLAN_B200_H_ */

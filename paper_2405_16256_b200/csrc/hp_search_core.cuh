@@ -1,0 +1,285 @@
+// hp_search_core.cuh — per-candidate and per-leaf search logic, shared by
+// the sm_100a kernels (hp_kernels.cu) and the CPU emulation test harness
+// (tests/emu). Pure functions of their arguments; no CUDA intrinsics.
+#pragma once
+
+#include "hp_core.cuh"
+
+namespace hpc {
+
+// Result codes stored per candidate slot.
+constexpr double T_INVALID = -2.0;   // neighbour with a count < 1 (planner.cpp:478)
+constexpr double T_MEMORY = -1.0;    // memory-pruned (planner.cpp:509-515)
+
+// ------------------------------------------------------------ candidate setup
+
+// Per-stage setup of one candidate (make_plan + memory gate + plan_stage_times,
+// planner.cpp:499-517, evaluate.cpp:23-76). Returns false when the stage's
+// memory exceeds the budget. hop[] is this leaf's row of hop times per link.
+HPD bool stage_setup(const Consts& c, const Leaf& lf, const LeafGroup* lg, const uint8_t* slots,
+                     const double* hop, int i, int count, StageDur& d) {
+  const LeafGroup& row = lg[slots[i]];
+  const int g = row.group;
+  const int P = lf.P;
+  stage_compute(c, row, i, P, count, d);
+  d.sf = 0.0;
+  d.sb = 0.0;
+  if (i + 1 < P) {
+    int h = lg[slots[i + 1]].group;
+    d.sf = hop[c.link_pair[g][h]];
+  }
+  if (i > 0) {
+    int h = lg[slots[i - 1]].group;
+    d.sb = hop[c.link_pair[h][g]];
+  }
+  d.dps = dp_sync(row, lf.dp, count);
+  double need = stage_memory(c, count, row.tp, (double)lf.B, in_flight(c, i, P, lf.M));
+  return !(need > c.budget[g]);
+}
+
+// Serial level-synchronous simulation of one candidate (all stages in one
+// thread). Used by the small-P thread-per-candidate kernel and the tests.
+// st/dur are caller scratch of P entries. Returns iteration_time_s
+// (evaluate.cpp:90-97).
+HPD double simulate_serial(bool gpipe, int P, int M, const StageDur* dur, StageState* st) {
+  for (int i = 0; i < P; ++i) stage_init(st[i]);
+  double max_end = 0.0;
+  int done = 0;
+  while (done < P) {
+    // previous-level snapshot of the neighbours: process stages in
+    // descending order so stage i-1 is still at its previous level when
+    // stage i reads it; stage i+1's previous values are kept in (pchb, pnb).
+    double pchb = 0.0;
+    int pnb = 0;
+    done = 0;
+    for (int i = P - 1; i >= 0; --i) {
+      double my_chb = st[i].chb;
+      int my_nb = st[i].nb;
+      int w = gpipe ? M : (P - i < M ? P - i : M);
+      double lchf = i > 0 ? st[i - 1].chf : 0.0;
+      int lnf = i > 0 ? st[i - 1].nf : 0;
+      stage_level(gpipe, i, P, M, w, dur[i], st[i], lchf, lnf, pchb, pnb, max_end);
+      pchb = my_chb;
+      pnb = my_nb;
+      done += stage_done(st[i], M) ? 1 : 0;
+    }
+  }
+  double iteration = 0.0;
+  for (int i = 0; i < P; ++i) iteration = dmax(iteration, st[i].free_t + dur[i].dps);
+  return dmax(max_end, iteration);
+}
+
+// ------------------------------------------------------------ seeds
+
+// Uniform and proportional seed splits of one leaf (planner.cpp:435-451):
+// split_layers(L, 1...1) and split_layers(L, stage_weights(blocks)).
+// w/frac: P doubles, order: P ints scratch.
+HPD void seed_splits(const Consts& c, const Leaf& lf, const LeafGroup* lg, const uint8_t* slots,
+                     int* uni, int* prop, double* w, double* frac, int* order) {
+  const int P = lf.P;
+  for (int i = 0; i < P; ++i) w[i] = 1.0;
+  split_layers(c.L, w, P, uni, frac, order);
+  double sum = 0.0;
+  for (int i = 0; i < P; ++i) {
+    w[i] = lg[slots[i]].weight;
+    sum += w[i];
+  }
+  for (int i = 0; i < P; ++i) w[i] /= sum;
+  split_layers(c.L, w, P, prop, frac, order);
+}
+
+HPD bool same_split(const int* a, const int* b, int P) {
+  for (int i = 0; i < P; ++i)
+    if (a[i] != b[i]) return false;
+  return true;
+}
+
+// better_than within/between leaves: (time, pp, encoding).
+HPD bool cand_less(const Consts& c, double ta, const Leaf& la, const LeafGroup* lga,
+                   const uint8_t* sa, const int* ca, double tb, const Leaf& lb,
+                   const LeafGroup* lgb, const uint8_t* sb, const int* cb) {
+  if (ta != tb) return ta < tb;
+  if (la.P != lb.P) return la.P < lb.P;
+  EncStream ea{&c, sa, lga, ca, la.P, (long long)la.M, la.B, la.dp, 0, 0, 0, 0, {0}, 0};
+  EncStream eb{&c, sb, lgb, cb, lb.P, (long long)lb.M, lb.B, lb.dp, 0, 0, 0, 0, {0}, 0};
+  return enc_less(ea, eb);
+}
+
+// ------------------------------------------------------------ hill climb
+
+// Per-leaf state of the steepest-descent search (planner.cpp:461-489) plus
+// the leaf's best candidate and its memo-equivalent counts.
+struct HillState {
+  double cur_time;
+  double best_time;
+  long long simulated;
+  long long pruned;
+  int steps;        // accepted moves (== path length)
+  int active;       // still climbing
+  int has_best;
+  int start;        // 0 none, 1 proportional, 2 uniform
+};
+
+// Move code of neighbour slot q: boundary b = q >> 1, d = +1 for even q,
+// -1 for odd q (planner.cpp:473-474 order: i ascending, +1 before -1).
+HPD int slot_of(int b, int d) { return 2 * b + (d > 0 ? 0 : 1); }
+
+// Seeds evaluated: init counts, best and the start point
+// (planner.cpp:434-468). t_uni/t_prop < 0 when memory-pruned.
+HPD void hill_init(const Consts& c, const Leaf& lf, const LeafGroup* lg, const uint8_t* slots,
+                   const int* uni, const int* prop, double t_uni, double t_prop, int* cur,
+                   int* best_split, HillState& hs, bool uniform_only) {
+  const int P = lf.P;
+  hs.simulated = 0;
+  hs.pruned = 0;
+  hs.steps = 0;
+  hs.has_best = 0;
+  hs.active = 0;
+  hs.start = 0;
+  hs.cur_time = 0.0;
+  hs.best_time = 0.0;
+  if (t_uni >= 0) {
+    hs.simulated++;
+    hs.has_best = 1;
+    hs.best_time = t_uni;
+    for (int i = 0; i < P; ++i) best_split[i] = uni[i];
+  } else {
+    hs.pruned++;
+  }
+  if (uniform_only) return;
+  bool prop_new = !same_split(uni, prop, P);
+  if (prop_new) {
+    if (t_prop >= 0) {
+      hs.simulated++;
+      if (!hs.has_best || cand_less(c, t_prop, lf, lg, slots, prop, hs.best_time, lf, lg, slots,
+                                    best_split)) {
+        hs.has_best = 1;
+        hs.best_time = t_prop;
+        for (int i = 0; i < P; ++i) best_split[i] = prop[i];
+      }
+    } else {
+      hs.pruned++;
+    }
+  }
+  if (lf.mode != 0) return;  // exhaustive leaves enumerate everything instead
+  if (t_prop >= 0) {
+    hs.start = 1;
+    hs.cur_time = t_prop;
+    for (int i = 0; i < P; ++i) cur[i] = prop[i];
+  } else if (t_uni >= 0) {
+    hs.start = 2;
+    hs.cur_time = t_uni;
+    for (int i = 0; i < P; ++i) cur[i] = uni[i];
+  }
+  hs.active = hs.start != 0 && 4 * c.L > 0;
+}
+
+// Marks old[q] for neighbours of cur that the reference's memo already holds
+// (planner.cpp:425-432): the seeds, path points and neighbourhoods of earlier
+// path points. Along a strictly improving path a neighbour of c_k can only be
+// within distance 1 of c_j (j < k) in prefix-sum space when
+// ||S_k - S_j||_1 <= 2, found by scanning the move history backwards.
+// delta: P ints scratch (zeroed on entry and exit).
+HPD void mark_old(const Leaf& lf, const int* cur, const int* uni, const int* prop,
+                  const short* hist, int steps, int* delta, unsigned char* old) {
+  const int P = lf.P;
+  const int nslots = 2 * (P - 1);
+  for (int q = 0; q < nslots; ++q) old[q] = 0;
+  // history scan: after applying moves t..k-1, delta = S_k - S_t
+  int D = 0;
+  for (int t = steps - 1; t >= 0; --t) {
+    int code = hist[t];
+    int b = code >> 1;
+    int d = (code & 1) ? -1 : 1;
+    int before = delta[b] < 0 ? -delta[b] : delta[b];
+    delta[b] += d;
+    int after = delta[b] < 0 ? -delta[b] : delta[b];
+    D += after - before;
+    if (D <= 2) {
+      if (D == 0) {
+        for (int q = 0; q < nslots; ++q) old[q] = 1;
+      } else {
+        for (int bb = 0; bb + 1 < P; ++bb) {
+          if (delta[bb] == 0) continue;
+          // moving boundary bb toward c_t: d' = -sign(delta)
+          old[slot_of(bb, delta[bb] > 0 ? -1 : 1)] = 1;
+        }
+      }
+    }
+  }
+  for (int t = 0; t < steps; ++t) delta[hist[t] >> 1] = 0;
+  // seeds: a neighbour equal to uniform / proportional
+  for (int s = 0; s < 2; ++s) {
+    const int* ref = s == 0 ? uni : prop;
+    int dist = 0, cb = -1, cd = 0;
+    int sc = 0, sr = 0;
+    for (int bb = 0; bb + 1 < P; ++bb) {
+      sc += cur[bb];
+      sr += ref[bb];
+      int dd = sc - sr;
+      if (dd != 0) {
+        dist += dd < 0 ? -dd : dd;
+        cb = bb;
+        cd = dd;
+      }
+    }
+    if (dist == 1) old[slot_of(cb, cd > 0 ? -1 : 1)] = 1;
+  }
+}
+
+// One steepest-descent step of a leaf given its neighbours' times
+// (planner.cpp:470-489). nb[q]: time, T_MEMORY or T_INVALID. Updates
+// counts, the leaf best, the current point and the history.
+HPD void hill_step(const Consts& c, const Leaf& lf, const LeafGroup* lg, const uint8_t* slots,
+                   int* cur, const int* uni, const int* prop, int* best_split, short* hist,
+                   HillState& hs, const double* nb, int* delta, unsigned char* old, int* tmp) {
+  const int P = lf.P;
+  const int nslots = 2 * (P - 1);
+  mark_old(lf, cur, uni, prop, hist, hs.steps, delta, old);
+  int bq = -1;
+  double bt = 0.0;
+  for (int q = 0; q < nslots; ++q) {
+    double t = nb[q];
+    if (t == T_INVALID) continue;
+    if (!old[q]) {
+      if (t >= 0) hs.simulated++;
+      else hs.pruned++;
+    }
+    if (t < 0) continue;
+    if (bq < 0 || t < bt) {
+      bq = q;
+      bt = t;
+    }
+    if (!old[q]) {
+      bool better = !hs.has_best || t < hs.best_time;
+      if (!better && t == hs.best_time) {
+        int b = q >> 1, d = (q & 1) ? -1 : 1;
+        for (int i = 0; i < P; ++i) tmp[i] = cur[i];
+        tmp[b] += d;
+        tmp[b + 1] -= d;
+        better = cand_less(c, t, lf, lg, slots, tmp, hs.best_time, lf, lg, slots, best_split);
+      }
+      if (better) {
+        int b = q >> 1, d = (q & 1) ? -1 : 1;
+        hs.has_best = 1;
+        hs.best_time = t;
+        for (int i = 0; i < P; ++i) best_split[i] = cur[i];
+        best_split[b] += d;
+        best_split[b + 1] -= d;
+      }
+    }
+  }
+  if (bq < 0 || !(bt < hs.cur_time)) {
+    hs.active = 0;
+    return;
+  }
+  int b = bq >> 1, d = (bq & 1) ? -1 : 1;
+  cur[b] += d;
+  cur[b + 1] -= d;
+  hist[hs.steps] = (short)bq;
+  hs.steps++;
+  hs.cur_time = bt;
+  if (hs.steps >= 4 * c.L) hs.active = 0;
+}
+
+}  // namespace hpc

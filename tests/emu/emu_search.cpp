@@ -1,0 +1,125 @@
+// TEST HARNESS ONLY — CPU emulation of the GPU search decomposition.
+//
+// Drives the exact per-candidate / per-leaf functions the sm_100a kernels run
+// (paper_2405_16256_b200/csrc/hp_search_core.cuh) in plain loops on the host,
+// so the algorithmic decomposition (level-synchronous simulator, on-device
+// seed splits, memo-equivalent hill-climb counting, exact tie-break) can be
+// checked against the reference oracle on CPU before it ever reaches a GPU.
+// Never linked into the product library.
+#include <cstring>
+#include <vector>
+
+#include "../../paper_2405_16256_b200/csrc/hp_host.hpp"
+#include "../../paper_2405_16256_b200/csrc/hp_search_core.cuh"
+
+using namespace hpc;
+
+namespace {
+
+struct LeafDev {
+  Leaf lf;
+  std::vector<LeafGroup> lg;
+  const uint8_t* slots;
+  const double* hop;
+};
+
+double eval(const Consts& c, const LeafDev& L, const int* split) {
+  const int P = L.lf.P;
+  std::vector<StageDur> d(P);
+  std::vector<StageState> st(P);
+  for (int i = 0; i < P; ++i) {
+    if (split[i] < 1) return T_INVALID;
+  }
+  for (int i = 0; i < P; ++i)
+    if (!stage_setup(c, L.lf, L.lg.data(), L.slots, L.hop, i, split[i], d[i])) return T_MEMORY;
+  return simulate_serial(c.schedule == 0, P, L.lf.M, d.data(), st.data());
+}
+
+}  // namespace
+
+extern "C" int emu_search(const hp_problem* in, hp_result* res) {
+  hph::Problem p;
+  hph::Status s = hph::load_problem(in, p);
+  if (!s.ok()) return s.code;
+  if (p.pruning) return HP_INTERNAL;  // emulation covers full mode
+  hph::enumerate(p);
+  Consts c;
+  hph::fill_consts(p, c);
+  const int G = c.n_groups;
+  std::vector<double> hop(p.mbs.size() * p.links.size());
+  for (size_t b = 0; b < p.mbs.size(); ++b)
+    for (size_t l = 0; l < p.links.size(); ++l) hop[b * p.links.size() + l] = hph::hop_time(p, (int)l, p.mbs[b]);
+  std::memset(res, 0, sizeof(*res));
+  res->tasks = (long long)p.tasks.size();
+  for (const hph::Task& t : p.tasks)
+    if (t.no_link) { res->candidates_pruned++; res->reason_counts[HP_REASON_NO_LINK]++; }
+    else if (t.leaf_begin == t.leaf_end) { res->candidates_pruned++; res->reason_counts[HP_REASON_NO_ASSIGNMENT]++; }
+
+  bool have = false;
+  double best_t = 0;
+  LeafDev best_leaf;
+  std::vector<int> best_split;
+  int best_li = -1;
+  for (int li = 0; li < (int)p.leaves.size(); ++li) {
+    const hph::LeafHost& h = p.leaves[li];
+    const hph::Task& t = p.tasks[h.task];
+    LeafDev L;
+    L.lf = Leaf{h.task, t.pp, (int)h.M, h.dp, h.B, h.B_idx, t.layout_off, 0, 0,
+                p.uniform_only ? 2 : (h.exhaustive ? 1 : 0), 0};
+    for (int g = 0; g < G; ++g) L.lg.push_back(hph::leaf_group(p, g, h.tp[g], h.B, h.dp, h.nodes[g]));
+    L.slots = &p.layouts[t.layout_off];
+    L.hop = &hop[h.B_idx * p.links.size()];
+    const int P = t.pp;
+    std::vector<int> uni(P), prop(P), cur(P), bs(P), order(P), delta(P, 0), tmp(P);
+    std::vector<double> w(P), frac(P), nb(2 * P);
+    std::vector<short> hist(4 * c.L + 1);
+    std::vector<unsigned char> old(2 * P);
+    HillState hs;
+    seed_splits(c, L.lf, L.lg.data(), L.slots, uni.data(), prop.data(), w.data(), frac.data(), order.data());
+    if (L.lf.mode == 1) {
+      hs.simulated = hs.pruned = 0;
+      hs.has_best = 0;
+      std::vector<int> comp(P);
+      unrank_composition(0, c.L, P, comp.data());
+      do {
+        double tt = eval(c, L, comp.data());
+        if (tt >= 0) {
+          hs.simulated++;
+          if (!hs.has_best || cand_less(c, tt, L.lf, L.lg.data(), L.slots, comp.data(), hs.best_time,
+                                        L.lf, L.lg.data(), L.slots, bs.data())) {
+            hs.has_best = 1; hs.best_time = tt; bs = comp;
+          }
+        } else hs.pruned++;
+      } while (next_composition(comp.data(), P));
+    } else {
+      double tu = eval(c, L, uni.data());
+      double tp = L.lf.mode == 2 ? -1 : eval(c, L, prop.data());
+      hill_init(c, L.lf, L.lg.data(), L.slots, uni.data(), prop.data(), tu, tp, cur.data(), bs.data(),
+                hs, L.lf.mode == 2);
+      while (hs.active) {
+        for (int q = 0; q < 2 * (P - 1); ++q) {
+          int b = q >> 1, d = (q & 1) ? -1 : 1;
+          tmp = cur;
+          tmp[b] += d; tmp[b + 1] -= d;
+          nb[q] = eval(c, L, tmp.data());
+        }
+        hill_step(c, L.lf, L.lg.data(), L.slots, cur.data(), uni.data(), prop.data(), bs.data(),
+                  hist.data(), hs, nb.data(), delta.data(), old.data(), tmp.data());
+      }
+    }
+    res->candidates_simulated += hs.simulated;
+    res->candidates_pruned += hs.pruned;
+    res->reason_counts[HP_REASON_MEMORY] += hs.pruned;
+    res->leaves++;
+    if (hs.has_best && (!have || cand_less(c, hs.best_time, L.lf, L.lg.data(), L.slots, bs.data(), best_t,
+                                           best_leaf.lf, best_leaf.lg.data(), best_leaf.slots, best_split.data()))) {
+      have = true; best_t = hs.best_time; best_leaf = L; best_split = bs; best_li = li;
+    }
+  }
+  if (!have) return HP_INFEASIBLE;
+  res->has_best = 1;
+  res->best_time_s = best_t;
+  res->best_pp = best_leaf.lf.P;
+  hph::make_plan(p, p.leaves[best_li], best_split.data(), res->best_plan);
+  return HP_OK;
+}
