@@ -1,0 +1,177 @@
+// hp_capi.cpp — the C ABI (include/hetplan_b200.h) over the host model and
+// the sm_100a kernels. No exception crosses this boundary.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+
+#include "../../include/hetplan_b200.h"
+#include "hp_device.hpp"
+#include "hp_host.hpp"
+
+struct hp_ctx {
+  hpd::Arena arena;
+  std::string err;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+hp_status fail(hp_ctx* ctx, const hph::Status& s) {
+  if (ctx) ctx->err = s.msg;
+  return s.code;
+}
+
+hp_status fail(hp_ctx* ctx, hp_status code, const std::string& m) {
+  return fail(ctx, hph::Status{code, m});
+}
+
+hp_status prepare(hp_ctx* ctx, const hp_problem* problem, hph::Problem& p) {
+  hph::Status s = hph::load_problem(problem, p);
+  if (!s.ok()) return fail(ctx, s);
+  hph::enumerate(p);
+  for (const hph::LeafHost& lf : p.leaves)
+    if (lf.M > 5000000) return fail(ctx, HP_INTERNAL, "simulate: micro_batches too large");
+  return HP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hp_abi_version(void) { return HP_ABI_VERSION; }
+
+hp_status hp_create(hp_ctx** out, int device) {
+  if (!out) return HP_INTERNAL;
+  *out = nullptr;
+  hp_ctx* ctx = new hp_ctx();
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->arena.sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->arena.stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return HP_CUDA;
+  }
+  ctx->arena.device = device;
+  *out = ctx;
+  return HP_OK;
+}
+
+void hp_destroy(hp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->arena.device);
+  ctx->arena.release();
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->arena.stream) cudaStreamDestroy(ctx->arena.stream);
+  delete ctx;
+}
+
+const char* hp_last_error(const hp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+hp_status hp_validate(hp_ctx* ctx, const hp_problem* problem) {
+  hph::Problem p;
+  hph::Status s = hph::load_problem(problem, p);
+  return s.ok() ? HP_OK : fail(ctx, s);
+}
+
+hp_status hp_probe(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts* opts,
+                   double* bound) {
+  (void)opts;
+  (void)problem;
+  if (bound) *bound = std::numeric_limits<double>::infinity();
+  return fail(ctx, HP_INTERNAL, "hp_probe: default (pruned) mode not built yet");
+}
+
+hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts* opts,
+                    hp_result* result) {
+  if (!ctx || !result) return HP_INTERNAL;
+  cudaSetDevice(ctx->arena.device);
+  std::memset(result, 0, sizeof(*result));
+  hph::Problem p;
+  hp_status st = prepare(ctx, problem, p);
+  if (st != HP_OK) return st;
+  int shard = opts ? opts->shard_index : 0;
+  int nshard = opts && opts->shard_count > 0 ? opts->shard_count : 1;
+  if (shard < 0 || shard >= nshard) return fail(ctx, HP_BAD_CONFIG, "bad shard index");
+  result->tasks = static_cast<int64_t>(p.tasks.size());
+  result->global_bound = std::numeric_limits<double>::infinity();
+  if (p.pruning) return fail(ctx, HP_INTERNAL, "default (pruned) mode not built yet");
+
+  // Task-level prunes (planner.cpp:317-327, 395-400) are host decisions;
+  // shard 0 reports them.
+  if (shard == 0) {
+    for (const hph::Task& t : p.tasks) {
+      if (t.no_link) {
+        result->candidates_pruned++;
+        result->reason_counts[HP_REASON_NO_LINK]++;
+      } else if (t.leaf_begin == t.leaf_end) {
+        result->candidates_pruned++;
+        result->reason_counts[HP_REASON_NO_ASSIGNMENT]++;
+      }
+    }
+  }
+  std::vector<int> mine = hph::shard_leaves(p, shard, nshard);
+  hpd::SearchOut out;
+  cudaEventRecord(ctx->ev0, ctx->arena.stream);
+  hph::Status s = hpd::search_full(ctx->arena, p, mine, out);
+  if (!s.ok()) return fail(ctx, s);
+  cudaEventRecord(ctx->ev1, ctx->arena.stream);
+  cudaEventSynchronize(ctx->ev1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  result->device_ms = ms;
+  result->gpu_launches = out.launches;
+  result->leaves = static_cast<int64_t>(mine.size());
+  result->candidates_simulated += out.simulated;
+  result->candidates_pruned += out.pruned;
+  result->reason_counts[HP_REASON_MEMORY] += out.pruned;
+  if (out.has_best) {
+    result->has_best = 1;
+    result->best_time_s = out.best_time;
+    const hph::LeafHost& lf = p.leaves[out.best_leaf];
+    result->best_pp = p.tasks[lf.task].pp;
+    hph::make_plan(p, lf, out.best_split.data(), result->best_plan);
+  }
+  return HP_OK;
+}
+
+int hp_better_than(const hp_problem* problem, double time_a, const hp_plan* plan_a, double time_b,
+                   const hp_plan* plan_b) {
+  hph::Problem p;
+  if (!hph::load_problem(problem, p).ok() || !plan_a || !plan_b) return 0;
+  return hph::compare_plans(p, time_a, *plan_a, time_b, *plan_b);
+}
+
+hp_status hp_evaluate_plans(hp_ctx* ctx, const hp_problem* problem, const hp_plan* plans,
+                            int32_t n, double* iteration_time_s) {
+  if (!ctx) return HP_INTERNAL;
+  cudaSetDevice(ctx->arena.device);
+  hph::Problem p;
+  hph::Status s = hph::load_problem(problem, p);
+  if (!s.ok()) return fail(ctx, s);
+  if (n < 0 || (n > 0 && (!plans || !iteration_time_s))) return fail(ctx, HP_BAD_CONFIG, "bad plan array");
+  for (int k = 0; k < n; ++k) {
+    const hp_plan& pl = plans[k];
+    if (pl.n_stages < 1 || pl.n_stages > HP_MAX_STAGES) return fail(ctx, HP_BAD_CONFIG, "plan: bad stage count");
+    if (pl.micro_batches_per_dp_replica < 1) return fail(ctx, HP_BAD_CONFIG, "simulate: micro_batches must be >= 1");
+    if (pl.micro_batches_per_dp_replica > 5000000) return fail(ctx, HP_BAD_CONFIG, "simulate: micro_batches too large");
+    for (int i = 0; i < pl.n_stages; ++i) {
+      const hp_stage& st = pl.stages[i];
+      if (st.group < 0 || st.group >= static_cast<int>(p.groups.size()))
+        return fail(ctx, HP_BAD_CONFIG, "plan: unknown device group");
+      if (st.tp_degree < 1) return fail(ctx, HP_BAD_CONFIG, "compute_time: tp_degree must be >= 1");
+      if (i + 1 < pl.n_stages && st.group != pl.stages[i + 1].group &&
+          p.pair[st.group][pl.stages[i + 1].group] < 0)
+        return fail(ctx, HP_BAD_CONFIG, "no link between stages " + std::to_string(i) + " and " + std::to_string(i + 1));
+    }
+  }
+  s = hpd::evaluate_plans(ctx->arena, p, plans, n, iteration_time_s);
+  return s.ok() ? HP_OK : fail(ctx, s);
+}
+
+}  // extern "C"

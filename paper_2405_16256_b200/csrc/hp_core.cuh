@@ -57,7 +57,7 @@ struct LeafGroup {
   int tp;
   int nodes;
   int group;
-  int pad;
+  int dp;          // StageAssignment.dp_degree
 };
 
 // One leaf of the search tree: (task, dp, B, per-group tp), planner.cpp:353-391.
@@ -71,7 +71,7 @@ struct Leaf {
   int layout_off;   // stage -> group bytes of the task
   int split_off;    // offset of this leaf's P-int rows in per-leaf split buffers
   int lg_off;       // offset of this leaf's LeafGroup rows (n_groups each)
-  int mode;         // 0 = hill climb, 1 = exhaustive
+  int mode;         // 0 hill climb, 1 exhaustive, 2 uniform only, 3 explicit plan
   int pad;
 };
 
@@ -111,8 +111,8 @@ HPD void stage_compute(const Consts& c, const LeafGroup& g, int i, int P, int co
 }
 
 // DP gradient sync of a stage, evaluate.cpp:65-73 + collective_time.
-HPD double dp_sync(const LeafGroup& g, int dp, int count) {
-  if (dp <= 1) return 0.0;
+HPD double dp_sync(const LeafGroup& g, int count) {
+  if (g.dp <= 1) return 0.0;
   double grad = (double)count * g.pbytes / g.tp;
   double moved = g.ar_mf * grad;
   return g.ar_lat + moved * 8.0 / g.ar_den;

@@ -355,6 +355,7 @@ hpc::LeafGroup leaf_group(const Problem& p, int g, int tp, int64_t B, int dp, in
   r.tp = tp;
   r.nodes = nodes;
   r.group = g;
+  r.dp = dp;
   return r;
 }
 

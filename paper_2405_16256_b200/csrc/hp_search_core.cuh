@@ -32,7 +32,8 @@ HPD bool stage_setup(const Consts& c, const Leaf& lf, const LeafGroup* lg, const
     int h = lg[slots[i - 1]].group;
     d.sb = hop[c.link_pair[h][g]];
   }
-  d.dps = dp_sync(row, lf.dp, count);
+  d.dps = dp_sync(row, count);
+  if (lf.mode == 3) return true;  // evaluate_plan_unchecked has no memory gate
   double need = stage_memory(c, count, row.tp, (double)lf.B, in_flight(c, i, P, lf.M));
   return !(need > c.budget[g]);
 }

@@ -1,0 +1,183 @@
+"""Host-side mirror of the reference planner interface for the hot path.
+
+    search(docs, jobs=1) -> SearchOutcome          (planner.hpp:115-116)
+    evaluate_plans(docs, plans) -> [iteration_time_s]  (evaluate.hpp:56-58, batched)
+
+`docs` are the reference's own JSON documents {"model","cluster","train",
+"planner"} (json_io.cpp:83-219). Errors raise the reference's exception kinds
+(ConfigError / InfeasibleError, errors.hpp:26-44). The work runs in the
+sm_100a CUDA library through the C ABI of include/hetplan_b200.h; there is no
+CPU fallback. Multi-GPU: search_sharded() runs one shard per rank and reduces
+the per-rank best records with one NCCL all-gather (torch.distributed).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+from . import abi
+from ._lib import lib
+
+
+@dataclass
+class SearchOutcome:
+    plan: dict
+    iteration_time_s: float
+    candidates_simulated: int
+    candidates_pruned: int
+    reason_counts: Dict[str, int] = field(default_factory=dict)
+    device_ms: float = 0.0
+    gpu_launches: int = 0
+    leaves: int = 0
+    tasks: int = 0
+    global_bound: float = math.inf
+    raw: Optional[abi.hp_result] = None
+
+
+class Engine:
+    """One hp_ctx bound to one CUDA device (reused across searches)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = lib()
+        self._ctx = C.c_void_p()
+        st = self._lib.hp_create(C.byref(self._ctx), device)
+        if st != abi.HP_OK:
+            raise RuntimeError(f"hp_create(device={device}) failed with status {st}")
+        self.device = device
+
+    def close(self):
+        if self._ctx:
+            self._lib.hp_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _raise(self, st: int, what: str):
+        msg = (self._lib.hp_last_error(self._ctx) or b"").decode()
+        if st == abi.HP_BAD_CONFIG:
+            raise abi.ConfigError(msg)
+        if st == abi.HP_INFEASIBLE:
+            raise abi.InfeasibleError(msg or "no feasible plan found")
+        raise RuntimeError(f"{what} failed (status {st}): {msg}")
+
+    def search_shard(self, problem: abi.Problem, shard_index: int = 0, shard_count: int = 1,
+                     global_bound: Optional[float] = None) -> abi.hp_result:
+        opts = abi.hp_search_opts(shard_index, shard_count, int(global_bound is not None), 0,
+                                  global_bound if global_bound is not None else 0.0)
+        res = abi.hp_result()
+        st = self._lib.hp_search(self._ctx, problem.ptr(), C.byref(opts), C.byref(res))
+        if st != abi.HP_OK:
+            self._raise(st, "hp_search")
+        return res
+
+    def probe_shard(self, problem: abi.Problem, shard_index: int = 0, shard_count: int = 1) -> float:
+        opts = abi.hp_search_opts(shard_index, shard_count, 0, 0, 0.0)
+        b = C.c_double()
+        st = self._lib.hp_probe(self._ctx, problem.ptr(), C.byref(opts), C.byref(b))
+        if st != abi.HP_OK:
+            self._raise(st, "hp_probe")
+        return b.value
+
+    def evaluate_plans(self, problem: abi.Problem, plans: List[abi.hp_plan]) -> List[float]:
+        n = len(plans)
+        arr = (abi.hp_plan * max(1, n))(*plans)
+        out = (C.c_double * max(1, n))()
+        st = self._lib.hp_evaluate_plans(self._ctx, problem.ptr(), arr, n, out)
+        if st != abi.HP_OK:
+            self._raise(st, "hp_evaluate_plans")
+        return list(out)[:n]
+
+
+_engines: Dict[int, Engine] = {}
+
+
+def engine(device: int = 0) -> Engine:
+    if device not in _engines:
+        _engines[device] = Engine(device)
+    return _engines[device]
+
+
+def _outcome(problem: abi.Problem, res: abi.hp_result) -> SearchOutcome:
+    return SearchOutcome(plan=problem.plan_to_doc(res.best_plan), iteration_time_s=res.best_time_s,
+                         candidates_simulated=res.candidates_simulated,
+                         candidates_pruned=res.candidates_pruned,
+                         reason_counts={k: int(res.reason_counts[i]) for i, k in enumerate(abi.REASONS)},
+                         device_ms=res.device_ms, gpu_launches=res.gpu_launches, leaves=res.leaves,
+                         tasks=res.tasks, global_bound=res.global_bound, raw=res)
+
+
+def search(docs: Dict[str, dict], jobs: int = 1, device: int = 0) -> SearchOutcome:
+    """search() of planner.hpp:115-116 on one GPU (`jobs` is accepted for
+    signature parity; the GPU replaces the thread pool)."""
+    problem = abi.Problem(docs)
+    res = engine(device).search_shard(problem)
+    if not res.has_best:
+        raise abi.InfeasibleError("no feasible plan found")
+    return _outcome(problem, res)
+
+
+def evaluate_plans(docs: Dict[str, dict], plans: List[dict], device: int = 0) -> List[float]:
+    problem = abi.Problem(docs)
+    return engine(device).evaluate_plans(problem, [problem.plan_from_doc(p) for p in plans])
+
+
+def reduce_results(problem: abi.Problem, results: List[abi.hp_result]) -> abi.hp_result:
+    """Deterministic reduction of per-shard results: counts add up, the best
+    record is picked with the reference's better_than (hp_better_than)."""
+    out = abi.hp_result()
+    l = lib()
+    for r in results:
+        out.candidates_simulated += r.candidates_simulated
+        out.candidates_pruned += r.candidates_pruned
+        for i in range(abi.HP_REASON_COUNT):
+            out.reason_counts[i] += r.reason_counts[i]
+        out.leaves += r.leaves
+        out.tasks = r.tasks
+        out.gpu_launches += r.gpu_launches
+        out.device_ms = max(out.device_ms, r.device_ms)
+        out.global_bound = r.global_bound
+        if r.has_best and (not out.has_best or l.hp_better_than(problem.ptr(), r.best_time_s, C.byref(r.best_plan),
+                                                                out.best_time_s, C.byref(out.best_plan)) < 0):
+            out.has_best = 1
+            out.best_time_s = r.best_time_s
+            out.best_pp = r.best_pp
+            C.memmove(C.byref(out.best_plan), C.byref(r.best_plan), C.sizeof(abi.hp_plan))
+    return out
+
+
+def search_sharded(docs: Dict[str, dict], rank: int, world: int, device: int, group=None) -> SearchOutcome:
+    """One shard per rank; the per-rank hp_result records (fixed size) are
+    all-gathered over NCCL/NVLink in one collective and every rank applies
+    the same exact reduction, so all ranks return the same plan."""
+    import torch
+    import torch.distributed as dist
+
+    problem = abi.Problem(docs)
+    eng = engine(device)
+    bound = None
+    if problem.struct.planner.time_bound_pruning:
+        b = eng.probe_shard(problem, rank, world)
+        t = torch.tensor([b], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        bound = float(t.item())
+    res = eng.search_shard(problem, rank, world, bound)
+    nbytes = C.sizeof(abi.hp_result)
+    mine = torch.frombuffer(bytearray(C.string_at(C.byref(res), nbytes)), dtype=torch.uint8).to(f"cuda:{device}")
+    gathered = torch.empty(world * nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+    dist.all_gather_into_tensor(gathered, mine, group=group)
+    host = gathered.cpu().numpy().tobytes()
+    recs = []
+    for r in range(world):
+        rec = abi.hp_result()
+        C.memmove(C.byref(rec), host[r * nbytes:(r + 1) * nbytes], nbytes)
+        recs.append(rec)
+    red = reduce_results(problem, recs)
+    if not red.has_best:
+        raise abi.InfeasibleError("no feasible plan found")
+    return _outcome(problem, red)
