@@ -151,11 +151,13 @@ typedef struct hp_plan {
  * (planner.cpp:640-651): a single-device search computes it itself; a
  * sharded search passes the min over shards of hp_probe() in global_bound
  * with have_global_bound = 1. */
+#define HP_FLAG_TIME_KERNELS 1 /* time every evaluator launch with CUDA events */
+
 typedef struct hp_search_opts {
   int32_t shard_index;
   int32_t shard_count;
   int32_t have_global_bound;
-  int32_t flags;       /* reserved, 0 */
+  int32_t flags;       /* HP_FLAG_* */
   double global_bound; /* used when have_global_bound */
 } hp_search_opts;
 
@@ -182,8 +184,16 @@ typedef struct hp_result {
   int32_t best_pp;
   double best_time_s;
   double global_bound;     /* probe bound used (inf when pruning is off) */
-  double device_ms;        /* kernel time of this call, CUDA events */
+  double device_ms;        /* device time of this call (first to last kernel), CUDA events */
   int64_t gpu_launches;    /* kernels this call launched */
+  int64_t eval_launches;   /* evaluator (k_eval*) launches among them */
+  double eval_ms;          /* summed evaluator kernel time (HP_FLAG_TIME_KERNELS) */
+  double eval_fp64_ops;    /* algorithmic FP64 add/max ops of simulated candidates */
+  double h2d_bytes;        /* host->device bytes copied by this call */
+  double d2h_bytes;        /* device->host bytes copied by this call */
+  double host_ms;          /* host enumeration + table build time */
+  int32_t hill_iterations; /* steepest-descent rounds */
+  int32_t _pad1;
   hp_plan best_plan;
 } hp_result;
 

@@ -22,6 +22,7 @@ HP_GPIPE, HP_1F1B = 0, 1
 HP_INTRA_NODE, HP_INTER_NODE, HP_INTER_GROUP = 0, 1, 2
 HP_GPU_DIRECT, HP_CPU_STAGED = 0, 1
 HP_REASON_COUNT = 4
+HP_FLAG_TIME_KERNELS = 1
 REASONS = ("memory", "bound", "no_link", "no_assignment")
 
 
@@ -87,7 +88,9 @@ class hp_result(C.Structure):
                 ("reason_counts", C.c_int64 * HP_REASON_COUNT), ("leaves", C.c_int64), ("tasks", C.c_int64),
                 ("has_best", C.c_int32), ("best_pp", C.c_int32), ("best_time_s", C.c_double),
                 ("global_bound", C.c_double), ("device_ms", C.c_double), ("gpu_launches", C.c_int64),
-                ("best_plan", hp_plan)]
+                ("eval_launches", C.c_int64), ("eval_ms", C.c_double), ("eval_fp64_ops", C.c_double),
+                ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double), ("host_ms", C.c_double),
+                ("hill_iterations", C.c_int32), ("_pad1", C.c_int32), ("best_plan", hp_plan)]
 
 
 class ConfigError(ValueError):

@@ -2,6 +2,7 @@
 // the sm_100a kernels. No exception crosses this boundary.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -92,6 +93,7 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   if (!ctx || !result) return HP_INTERNAL;
   cudaSetDevice(ctx->arena.device);
   std::memset(result, 0, sizeof(*result));
+  auto h0 = std::chrono::steady_clock::now();
   hph::Problem p;
   hp_status st = prepare(ctx, problem, p);
   if (st != HP_OK) return st;
@@ -116,6 +118,8 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
     }
   }
   std::vector<int> mine = hph::shard_leaves(p, shard, nshard);
+  result->host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+  ctx->arena.time_evals = opts && (opts->flags & HP_FLAG_TIME_KERNELS);
   hpd::SearchOut out;
   cudaEventRecord(ctx->ev0, ctx->arena.stream);
   hph::Status s = hpd::search_full(ctx->arena, p, mine, out);
@@ -126,6 +130,12 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   result->device_ms = ms;
   result->gpu_launches = out.launches;
+  result->eval_launches = out.eval_launches;
+  result->eval_ms = out.eval_ms;
+  result->eval_fp64_ops = out.eval_fp64_ops;
+  result->h2d_bytes = out.h2d_bytes;
+  result->d2h_bytes = out.d2h_bytes + sizeof(hp_result);
+  result->hill_iterations = out.hill_iterations;
   result->leaves = static_cast<int64_t>(mine.size());
   result->candidates_simulated += out.simulated;
   result->candidates_pruned += out.pruned;

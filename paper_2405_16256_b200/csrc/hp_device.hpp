@@ -18,6 +18,32 @@ struct Arena {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   std::map<std::string, std::pair<void*, size_t>> bufs;
+  // optional per-launch timing of the evaluator kernels (bench roofline)
+  bool time_evals = false;
+  double h2d_bytes = 0.0, d2h_bytes = 0.0;  // per search
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+
+  void event_pair(cudaEvent_t* e0, cudaEvent_t* e1) {
+    while (ev_pool.size() < ev_used + 2) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    *e0 = ev_pool[ev_used++];
+    *e1 = ev_pool[ev_used++];
+  }
+
+  // Sums the recorded pairs (caller synchronised the stream) and resets.
+  double drain_events() {
+    double ms = 0.0;
+    for (size_t k = 0; k + 1 < ev_used; k += 2) {
+      float x = 0.f;
+      if (cudaEventElapsedTime(&x, ev_pool[k], ev_pool[k + 1]) == cudaSuccess) ms += x;
+    }
+    ev_used = 0;
+    return ms;
+  }
 
   hph::Status get(const char* name, size_t bytes, void** out) {
     auto& e = bufs[name];
@@ -39,6 +65,8 @@ struct Arena {
     for (auto& kv : bufs)
       if (kv.second.first) cudaFree(kv.second.first);
     bufs.clear();
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+    ev_pool.clear();
   }
 };
 
@@ -51,6 +79,10 @@ struct SearchOut {
   long long launches = 0;
   int hill_iterations = 0;
   double global_bound = 0.0;
+  long long eval_launches = 0;
+  double eval_ms = 0.0;        // summed evaluator kernel time (when timed)
+  double eval_fp64_ops = 0.0;  // algorithmic FP64 add/max ops simulated
+  double h2d_bytes = 0.0, d2h_bytes = 0.0;
 };
 
 // Full strategy sweep (time_bound_pruning = false) over `my_leaves`.

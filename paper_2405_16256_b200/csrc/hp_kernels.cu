@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "hp_device.hpp"
@@ -67,6 +68,7 @@ struct Bufs {
   double* nb;
   double* xbuf;
   HillState* hs;
+  unsigned long long* ops;  // algorithmic FP64 add/max ops of simulated candidates
 };
 
 __device__ __forceinline__ int next_pow2(int v) {
@@ -87,6 +89,45 @@ __host__ __device__ inline int k_class(int P) {
   int k = (P + 31) / 32;
   return k < 1 ? 1 : k;
 }
+
+// Evaluator classes. 0..3: fast 1F1B kernel (closed-form level schedule,
+// needs M >= P) with K = 2,4,6,8 stages per lane; 4..7: generic
+// counter-driven kernel (GPipe, M < P) with K = 1,2,3,8.
+constexpr int NCLS = 8;
+
+__host__ __device__ inline int class_K(int cls) {
+  return cls < 4 ? 2 * (cls + 1) : (cls == 7 ? 8 : cls - 3);
+}
+
+// Lanes per candidate.
+__host__ __device__ inline int class_width(int cls, int P) {
+  int K = class_K(cls);
+  return cls < 4 ? (P + K - 1) / K : seg_width(P, K);
+}
+
+// Fast-kernel K maximising lane utilisation P*floor(32/W)/(32K), W = ceil(P/K).
+__host__ __device__ inline int fast_K(int P) {
+  int bestK = 8;
+  double bestU = -1.0;
+  for (int K = 2; K <= 8; K += 2) {
+    int W = (P + K - 1) / K;
+    if (W > 32) continue;
+    double u = (double)P * (32 / W) / (32.0 * K);
+    if (u > bestU + 1e-12) {
+      bestU = u;
+      bestK = K;
+    }
+  }
+  return bestK;
+}
+
+__host__ __device__ inline int eval_class(int P, int M, bool gpipe) {
+  if (!gpipe && M >= P && P <= 256) return fast_K(P) / 2 - 1;
+  int K = k_class(P);
+  return 4 + (K >= 4 ? 3 : K - 1);
+}
+
+__host__ __device__ inline int class_cpw(int cls, int P) { return 32 / class_width(cls, P); }
 
 // ------------------------------------------------------------------ seeds
 
@@ -110,7 +151,7 @@ __device__ __forceinline__ int cand_count(const Bufs& b, const Leaf& lf, const W
   if (w.kind == 1) {
     int q = (int)w.first + s;
     int mb = q >> 1, d = (q & 1) ? -1 : 1;
-    int c = b.cur[lf.split_off + i];
+    int c = __ldcg(b.cur + lf.split_off + i);  // written by another SM's hill step
     if (i == mb) c += d;
     if (i == mb + 1) c -= d;
     return c;
@@ -118,17 +159,11 @@ __device__ __forceinline__ int cand_count(const Bufs& b, const Leaf& lf, const W
   return 0;
 }
 
+// Generic evaluator (GPipe, M < P): counter-driven readiness per level.
 template <int K>
-__global__ void __launch_bounds__(256) k_eval(Bufs b, const Work* items, const int* n_items,
-                                              int* next_item) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void eval_item_generic(const Bufs& b, const Work& w, const int lane) {
   const bool gpipe = c_consts.schedule == 0;
-  for (;;) {
-    int it = 0;
-    if (lane == 0) it = atomicAdd(next_item, 1);
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= *n_items) return;
-    const Work w = items[it];
+  {
     const Leaf lf = b.leaves[w.leaf];
     const int P = lf.P;
     const int M = lf.M;
@@ -242,11 +277,343 @@ __global__ void __launch_bounds__(256) k_eval(Bufs b, const Work* items, const i
       if (w.kind == 0) b.tseed[2 * w.leaf + (int)w.first + seg] = t;
       else if (w.kind == 1) b.nb[b.nb_off[w.leaf] + (int)w.first + seg] = t;
       else b.xbuf[w.out + seg] = t;
+      if (run && b.ops) atomicAdd(b.ops, (unsigned long long)(8LL * P * M - 4LL * M));
     }
   }
 }
 
+// Fast 1F1B evaluator (M >= P). The unit-time ASAP level of every op has a
+// closed form (checked against the counter-driven schedule in tests):
+//   F(i,m) at level i+m (m < P-i, warm-up) or 2m+i (m >= P-i),
+//   B(i,j) at level 2P-1-i+2j,   T = 2(M+P-1) levels.
+// With an even number K of consecutive stages per lane, the F/B type of
+// local stage r in the steady state depends only on the parity of t - r, so
+// the whole warp follows one instruction stream (no divergence) and only the
+// warm-up/cool-down windows are predicated. Segments are packed at exact
+// width W = ceil(P/K) (floor(32/W) candidates per warp).
+template <int K>
+__device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, const int lane) {
+  const Leaf lf = b.leaves[w.leaf];
+  const int P = lf.P;
+  const int M = lf.M;
+  const int W = (P + K - 1) / K;
+  const int cpw = 32 / W;
+  const int seg = lane / W;
+  const int sl = lane - seg * W;
+  const bool has_cand = seg < cpw && seg < w.n;
+  const LeafGroup* lg = b.lg + lf.lg_off;
+  const uint8_t* slots = b.layouts + lf.layout_off;
+  const double* hop = b.hop + lf.B_idx * c_consts.n_links;
+  const double NEG = -__longlong_as_double(0x7ff0000000000000LL) * 1.0;  // -inf
+
+  double f[K], bw[K], sf[K], sb[K], dps[K];
+  bool valid = true, mem_ok = true;
+  int cnt[K];
+  if (w.kind == 2 && has_cand) {
+    long long rank = w.first + seg;
+    int rem = c_consts.L;
+    int last = min(P - 1, sl * K + K - 1);
+    for (int j = 0; j <= last; ++j) {
+      int v;
+      if (j == P - 1) {
+        v = rem;
+      } else {
+        int left = P - j;
+        for (v = 1;; ++v) {
+          long long cntv = binom(rem - v - 1, left - 2);
+          if (rank < cntv) break;
+          rank -= cntv;
+        }
+      }
+      rem -= v;
+      int r = j - sl * K;
+      if (r >= 0 && r < K) cnt[r] = v;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int i = sl * K + r;
+    f[r] = bw[r] = NEG;
+    sf[r] = sb[r] = 0.0;
+    dps[r] = 0.0;
+    if (has_cand && i < P) {
+      int c = w.kind == 2 ? cnt[r] : cand_count(b, lf, w, seg, i);
+      StageDur d;
+      if (c < 1) {
+        valid = false;
+      } else {
+        if (!stage_setup(c_consts, lf, lg, slots, hop, i, c, d)) mem_ok = false;
+        f[r] = d.f;
+        bw[r] = d.b;
+        // The last stage sends no activations forward and stage 0 no
+        // gradients backward (sim.cpp:127,137): a -inf hop keeps those
+        // channels at -inf, which doubles as the "no dependency" operand for
+        // the neighbouring segment / padding lanes (max(x, -inf) = x).
+        sf[r] = i == P - 1 ? NEG : d.sf;
+        sb[r] = i == 0 ? NEG : d.sb;
+        dps[r] = d.dps;
+      }
+    }
+  }
+  const unsigned segmask = (W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << (seg * W);
+  const unsigned inv = __ballot_sync(0xffffffffu, !valid) & segmask;
+  const unsigned mem = __ballot_sync(0xffffffffu, !mem_ok) & segmask;
+  const bool run = has_cand && inv == 0 && mem == 0;
+
+  // Lanes that do not simulate (padding, idle or pruned segments) hold -inf
+  // everywhere, so every exchange across a segment boundary reads -inf.
+  double fr[K], chf[K], chb[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int i = sl * K + r;
+    const bool real = run && i < P;
+    if (!real) {
+      f[r] = bw[r] = NEG;
+      sf[r] = sb[r] = 0.0;
+    }
+    fr[r] = real ? 0.0 : NEG;
+    chf[r] = (real && i != P - 1) ? 0.0 : NEG;
+    chb[r] = (real && i != 0) ? 0.0 : NEG;
+  }
+  const int src_l = (lane + 31) & 31;   // rotate: lane 0 reads lane 31 (-inf)
+  const int src_r = (lane + 1) & 31;
+  if (__any_sync(0xffffffffu, run)) {
+    // ---- warm-up, levels 0..P-1: stage i runs F(i, t-i) once t >= i
+    for (int t = 0; t < P; ++t) {
+      const double lchf = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
+#pragma unroll
+      for (int r = K - 1; r >= 0; --r) {  // descending: read chf[r-1] before it moves
+        const int i = sl * K + r;
+        const double recv = r == 0 ? lchf : chf[r > 0 ? r - 1 : 0];
+        const double nfr = dmax(fr[r], recv) + f[r];
+        const double nch = dmax(nfr, chf[r]) + sf[r];
+        if (i <= t) {
+          fr[r] = nfr;
+          chf[r] = nch;
+        }
+      }
+    }
+    const int T = 2 * (M + P - 1);
+    const int core_lo = 2 * P, core_hi = 2 * M - 2;  // every stage busy
+    // one edge (predicated) level
+    auto edge = [&](int t) {
+      const double lchf = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
+      const double rchb = __shfl_sync(0xffffffffu, chb[0], src_r);
+      double pchf[K], pchb[K];
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        pchf[r] = chf[r];
+        pchb[r] = chb[r];
+      }
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const int i = sl * K + r;
+        const bool isF = ((t - r) & 1) == 0;  // (t - i) even, i - r even
+        const bool act = isF ? (t >= 2 * P - i && t <= 2 * M - 2 + i)
+                             : (t >= 2 * P - 1 - i && t <= 2 * M + 2 * P - 3 - i);
+        const double recv = isF ? (r == 0 ? lchf : pchf[r > 0 ? r - 1 : 0])
+                                : (r == K - 1 ? rchb : pchb[r < K - 1 ? r + 1 : 0]);
+        const double nfr = dmax(fr[r], recv) + (isF ? f[r] : bw[r]);
+        const double nch = dmax(nfr, isF ? chf[r] : chb[r]) + (isF ? sf[r] : sb[r]);
+        if (act) {
+          fr[r] = nfr;
+          if (isF) chf[r] = nch;
+          else chb[r] = nch;
+        }
+      }
+    };
+    // one core level of parity PAR: stage r runs F iff (PAR - r) is even;
+    // neighbours run the opposite op, so no snapshot is needed.
+    auto core = [&](auto par_tag) {
+      constexpr int PAR = decltype(par_tag)::value;
+      const double lchf = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
+      const double rchb = __shfl_sync(0xffffffffu, chb[0], src_r);
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        if (((PAR - r) & 1) == 0) {
+          const double recv = r == 0 ? lchf : chf[r > 0 ? r - 1 : 0];
+          fr[r] = dmax(fr[r], recv) + f[r];
+          chf[r] = dmax(fr[r], chf[r]) + sf[r];
+        } else {
+          const double recv = r == K - 1 ? rchb : chb[r < K - 1 ? r + 1 : 0];
+          fr[r] = dmax(fr[r], recv) + bw[r];
+          chb[r] = dmax(fr[r], chb[r]) + sb[r];
+        }
+      }
+    };
+    int t = P;
+    for (; t < T && t < core_lo; ++t) edge(t);
+    if (core_lo <= core_hi) {
+      // core_lo is even: pairs (even, odd), then the final even level
+      for (; t + 1 <= core_hi; t += 2) {
+        core(std::integral_constant<int, 0>{});
+        core(std::integral_constant<int, 1>{});
+      }
+      if (t <= core_hi) {
+        core(std::integral_constant<int, 0>{});
+        ++t;
+      }
+    }
+    for (; t < T; ++t) edge(t);
+  }
+  double v = 0.0;
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int i = sl * K + r;
+    if (run && i < P) {
+      v = dmax(v, fr[r]);
+      v = dmax(v, chf[r]);
+      v = dmax(v, chb[r]);
+      v = dmax(v, fr[r] + dps[r]);
+    }
+  }
+  for (int off = 1; off < W; off <<= 1) {
+    double o = __shfl_down_sync(0xffffffffu, v, off);
+    if (sl + off < W) v = dmax(v, o);
+  }
+  if (sl == 0 && has_cand) {
+    double tt = inv ? T_INVALID : (mem ? T_MEMORY : v);
+    if (w.kind == 0) b.tseed[2 * w.leaf + (int)w.first + seg] = tt;
+    else if (w.kind == 1) b.nb[b.nb_off[w.leaf] + (int)w.first + seg] = tt;
+    else b.xbuf[w.out + seg] = tt;
+    if (run && b.ops) atomicAdd(b.ops, (unsigned long long)(8LL * P * M - 4LL * M));
+  }
+}
+
+template <int K, bool FAST>
+__device__ __forceinline__ void eval_item(const Bufs& b, const Work& w, const int lane) {
+  if constexpr (FAST) eval_item_fast<K>(b, w, lane);
+  else eval_item_generic<K>(b, w, lane);
+}
+
+// Batch evaluator: warps pull work items from a list.
+template <int K, bool FAST>
+__global__ void __launch_bounds__(256) k_eval(Bufs b, const Work* items, const int* n_items,
+                                              int* next_item) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(next_item, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= *n_items) return;
+    const Work w = items[it];
+    eval_item<K, FAST>(b, w, lane);
+  }
+}
+
 // ------------------------------------------------------------------ hill climb
+
+// Device-side work queue of the asynchronous steepest-descent search. Every
+// leaf advances on its own: the warp that finishes the last neighbour item of
+// a leaf runs that leaf's step (hill_step) and enqueues its next neighbours,
+// so there is no global per-step barrier and no host round trip; the kernel
+// ends when no leaf of its class is still climbing.
+struct AsyncQ {
+  Work* slots;
+  unsigned long long* seq;   // slot k holds ticket t when seq[k] == t + 1
+  unsigned long long* head;  // next ticket to consume
+  unsigned long long* tail;  // next ticket to produce
+  int* pending;              // per leaf: items of the current step not yet done
+  int* active;               // leaves of this class still climbing
+  unsigned long long cap;
+};
+
+__device__ void push_items(const Bufs& b, const AsyncQ& q, int li, int cls) {
+  const Leaf lf = b.leaves[li];
+  const int cpw = class_cpw(cls, lf.P);
+  const int nslots = 2 * (lf.P - 1);
+  const int nit = (nslots + cpw - 1) / cpw;
+  q.pending[li] = nit;
+  unsigned long long t = atomicAdd(q.tail, (unsigned long long)nit);
+  for (int j = 0; j < nit; ++j) {
+    Work w;
+    w.leaf = li;
+    w.kind = 1;
+    w.first = j * cpw;
+    w.n = min(cpw, nslots - j * cpw);
+    w.out = 0;
+    const unsigned long long k = (t + j) % q.cap;
+    q.slots[k] = w;
+    __threadfence();
+    atomicExch(q.seq + k, t + j + 1);
+  }
+}
+
+// Enqueue the first step of every climbing leaf of class `cls`.
+__global__ void k_async_seed(Bufs b, AsyncQ q, const int* ids, int n, int cls) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int li = ids[k];
+  if (!b.hs[li].active) return;
+  atomicAdd(q.active, 1);
+  push_items(b, q, li, cls);
+}
+
+template <int K, bool FAST>
+__global__ void __launch_bounds__(256) k_hill_async(Bufs b, AsyncQ q, int cls) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned long long h = 0;
+    int quit = 0;
+    Work w{};
+    if (lane == 0) {
+      h = atomicAdd(q.head, 1ULL);
+      const unsigned long long k = h % q.cap;
+      volatile unsigned long long* sq = q.seq + k;
+      unsigned ns = 32;
+      while (*sq != h + 1) {
+        if (*(volatile int*)q.active == 0) {
+          quit = 1;
+          break;
+        }
+        __nanosleep(ns);
+        if (ns < 2048) ns <<= 1;
+      }
+      if (!quit) {
+        __threadfence();
+        const Work* s = q.slots + k;
+        w.leaf = __ldcg(&s->leaf);
+        w.kind = __ldcg(&s->kind);
+        w.first = __ldcg(&s->first);
+        w.n = __ldcg(&s->n);
+      }
+    }
+    quit = __shfl_sync(0xffffffffu, quit, 0);
+    if (quit) return;
+    w.leaf = __shfl_sync(0xffffffffu, w.leaf, 0);
+    w.kind = __shfl_sync(0xffffffffu, w.kind, 0);
+    w.first = __shfl_sync(0xffffffffu, w.first, 0);
+    w.n = __shfl_sync(0xffffffffu, w.n, 0);
+    w.out = 0;
+    eval_item<K, FAST>(b, w, lane);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      if (atomicSub(q.pending + w.leaf, 1) == 1) {
+        __threadfence();
+        const int li = w.leaf;
+        const Leaf lf = b.leaves[li];
+        HillState hs = b.hs[li];
+        int delta[HP_MAX_STAGES];
+        unsigned char old[2 * HP_MAX_STAGES];
+        int tmp[HP_MAX_STAGES];
+        for (int i = 0; i < lf.P; ++i) delta[i] = 0;
+        hill_step(c_consts, lf, b.lg + lf.lg_off, b.layouts + lf.layout_off, b.cur + lf.split_off,
+                  b.uni + lf.split_off, b.prop + lf.split_off, b.best + lf.split_off,
+                  b.hist + b.hist_off[li], hs, b.nb + b.nb_off[li], delta, old, tmp);
+        b.hs[li] = hs;
+        if (hs.active) {
+          __threadfence();
+          push_items(b, q, li, cls);
+        } else {
+          __threadfence();
+          atomicSub(q.active, 1);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
 
 __global__ void k_hill_init(Bufs b, const int* leaf_ids, int n, int uniform_only, int* active,
                             int* n_active) {
@@ -264,14 +631,13 @@ __global__ void k_hill_init(Bufs b, const int* leaf_ids, int n, int uniform_only
 
 // Work items for the neighbours of every active leaf, bucketed by K class.
 __global__ void k_gen(Bufs b, const int* active, const int* n_active, Work* items, int cap,
-                      int* n_items /*[4]*/) {
+                      int* n_items /*[NCLS]*/) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= *n_active) return;
   int li = active[k];
   const Leaf lf = b.leaves[li];
-  int K = k_class(lf.P);
-  int cls = K >= 4 ? 3 : K - 1;
-  int cpw = 32 / seg_width(lf.P, K);
+  int cls = eval_class(lf.P, lf.M, c_consts.schedule == 0);
+  int cpw = class_cpw(cls, lf.P);
   int nslots = 2 * (lf.P - 1);
   int nit = (nslots + cpw - 1) / cpw;
   int base = atomicAdd(&n_items[cls], nit);
@@ -337,7 +703,7 @@ __global__ void k_exh_reduce(Bufs b, const ExhSpan* spans, int n_spans) {
     bool better = !hs.has_best || t < hs.best_time;
     if (!better && t == hs.best_time) {
       unrank_composition(sp.first + j, c_consts.L, lf.P, comp);
-      better = cand_less(c_consts, t, lf, lg, slots, comp, hs.best_time, lf, lg, slots, best);
+      better = split_enc_less(lf.P, comp, best);
     }
     if (better) {
       hs.has_best = 1;
@@ -424,6 +790,7 @@ static hph::Status upload(Arena& a, const char* name, const std::vector<T>& v, T
   hph::Status s = a.get(name, std::max<size_t>(1, v.size()) * sizeof(T), &p);
   if (!s.ok()) return s;
   if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, a.stream));
+  a.h2d_bytes += static_cast<double>(v.size() * sizeof(T));
   *out = static_cast<T*>(p);
   return s;
 }
@@ -436,13 +803,38 @@ static hph::Status scratch(Arena& a, const char* name, size_t n, T** out) {
   return s;
 }
 
-static void launch_eval(int K, const hpk::Bufs& b, const Work* items, const int* n_items,
+static void launch_eval(int cls, const hpk::Bufs& b, const Work* items, const int* n_items,
                         int* next, int grid, cudaStream_t st) {
-  switch (K) {
-    case 1: hpk::k_eval<1><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
-    case 2: hpk::k_eval<2><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
-    case 3: hpk::k_eval<3><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
-    default: hpk::k_eval<8><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
+  switch (cls) {
+    case 0: hpk::k_eval<2, true><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
+    case 1: hpk::k_eval<4, true><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
+    case 2: hpk::k_eval<6, true><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
+    case 3: hpk::k_eval<8, true><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
+    case 4: hpk::k_eval<1, false><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
+    case 5: hpk::k_eval<2, false><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
+    case 6: hpk::k_eval<3, false><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
+    default: hpk::k_eval<8, false><<<grid, 256, 0, st>>>(b, items, n_items, next); break;
+  }
+}
+
+template <int K, bool FAST>
+static int async_grid(int sm_count) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hpk::k_hill_async<K, FAST>, 256, 0);
+  return sm_count * (per_sm > 0 ? per_sm : 1);
+}
+
+static void launch_async(int cls, const hpk::Bufs& b, const hpk::AsyncQ& q, int sm_count,
+                         cudaStream_t st) {
+  switch (cls) {
+    case 0: hpk::k_hill_async<2, true><<<async_grid<2, true>(sm_count), 256, 0, st>>>(b, q, cls); break;
+    case 1: hpk::k_hill_async<4, true><<<async_grid<4, true>(sm_count), 256, 0, st>>>(b, q, cls); break;
+    case 2: hpk::k_hill_async<6, true><<<async_grid<6, true>(sm_count), 256, 0, st>>>(b, q, cls); break;
+    case 3: hpk::k_hill_async<8, true><<<async_grid<8, true>(sm_count), 256, 0, st>>>(b, q, cls); break;
+    case 4: hpk::k_hill_async<1, false><<<async_grid<1, false>(sm_count), 256, 0, st>>>(b, q, cls); break;
+    case 5: hpk::k_hill_async<2, false><<<async_grid<2, false>(sm_count), 256, 0, st>>>(b, q, cls); break;
+    case 6: hpk::k_hill_async<3, false><<<async_grid<3, false>(sm_count), 256, 0, st>>>(b, q, cls); break;
+    default: hpk::k_hill_async<8, false><<<async_grid<8, false>(sm_count), 256, 0, st>>>(b, q, cls); break;
   }
 }
 
@@ -454,6 +846,8 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   Consts c;
   hph::fill_consts(p, c);
   CK(cudaMemcpyToSymbolAsync(hpk::c_consts, &c, sizeof c, 0, cudaMemcpyHostToDevice, st));
+  a.h2d_bytes = sizeof c;
+  a.d2h_bytes = 0;
 
   // ---- host tables (split-independent, exact reference order)
   std::vector<Leaf> leaves(nL);
@@ -521,10 +915,28 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   if (!(s = scratch(a, "hs", nL, &b.hs)).ok()) return s;
   CK(cudaMemsetAsync(b.hs, 0, sizeof(HillState) * std::max(1, nL), st));
 
-  int* d_ctr;  // [0..3] item counts per class, [4..7] next counters, [8] n_active, [9] n_next
-  if (!(s = scratch(a, "ctr", 16, &d_ctr)).ok()) return s;
+  // counters: [0..7] items per class, [8..15] next-item per class,
+  // [16] n_active, [17] n_next, [18..19] one-off queue count / next
+  int* d_ctr;
+  if (!(s = scratch(a, "ctr", 32, &d_ctr)).ok()) return s;
+  unsigned long long* d_ops;
+  if (!(s = scratch(a, "ops", 1, &d_ops)).ok()) return s;
+  CK(cudaMemsetAsync(d_ops, 0, sizeof(unsigned long long), st));
+  b.ops = d_ops;
   const int grid = a.sm_count * 8;
   const int T = 128;
+
+  auto eval_launch = [&](int cls, const Work* items, const int* n_items, int* next) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (a.time_evals) {
+      a.event_pair(&e0, &e1);
+      cudaEventRecord(e0, st);
+    }
+    launch_eval(cls, b, items, n_items, next, grid, st);
+    if (a.time_evals) cudaEventRecord(e1, st);
+    out.launches++;
+    out.eval_launches++;
+  };
 
   // ---- seeds
   if (nL > 0) {
@@ -533,78 +945,91 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   }
 
   // ---- seed evaluation (uniform + proportional of hill / uniform-only leaves)
-  std::vector<std::vector<Work>> seedq(4);
+  std::vector<std::vector<Work>> seedq(hpk::NCLS);
+  const bool gpipe = p.schedule == HP_GPIPE;
   for (int k : hill_ids) {
-    int K = hpk::k_class(leaves[k].P);
-    int cls = K >= 4 ? 3 : K - 1;
-    int cpw = 32 / hpk::seg_width(leaves[k].P, K);
+    int cls = hpk::eval_class(leaves[k].P, leaves[k].M, gpipe);
+    int cpw = hpk::class_cpw(cls, leaves[k].P);
     int n = p.uniform_only ? 1 : 2;
     if (cpw >= n) {
       seedq[cls].push_back(Work{k, 0, 0, n, 0});
     } else {
-      // one candidate per work item
       seedq[cls].push_back(Work{k, 0, 0, 1, 0});
       if (n == 2) seedq[cls].push_back(Work{k, 0, 1, 1, 0});
     }
   }
   auto run_queues = [&](std::vector<std::vector<Work>>& qs, const char* tag) -> hph::Status {
-    for (int cls = 0; cls < 4; ++cls) {
+    for (int cls = 0; cls < hpk::NCLS; ++cls) {
       if (qs[cls].empty()) continue;
       Work* d_items;
       std::string nm = std::string(tag) + std::to_string(cls);
       hph::Status s2 = upload(a, nm.c_str(), qs[cls], &d_items);
       if (!s2.ok()) return s2;
       int cnt[2] = {static_cast<int>(qs[cls].size()), 0};
-      CK(cudaMemcpyAsync(d_ctr + 12, cnt, sizeof cnt, cudaMemcpyHostToDevice, st));
-      launch_eval(cls == 3 ? 8 : cls + 1, b, d_items, d_ctr + 12, d_ctr + 13, grid, st);
-      out.launches++;
-      CK(cudaStreamSynchronize(st));  // host count buffer reused per queue
+      CK(cudaMemcpyAsync(d_ctr + 18, cnt, sizeof cnt, cudaMemcpyHostToDevice, st));
+      eval_launch(cls, d_items, d_ctr + 18, d_ctr + 19);
+      CK(cudaStreamSynchronize(st));  // the one-off count slot is reused per queue
     }
     return hph::Status{};
   };
   if (!(s = run_queues(seedq, "seedq")).ok()) return s;
 
-  // ---- hill climb
-  int *d_ids, *d_act0, *d_act1;
+  // ---- hill climb: one asynchronous persistent launch per evaluator class
+  int* d_ids;
   std::vector<int> ids(hill_ids.begin(), hill_ids.end());
   if (!(s = upload(a, "hill_ids", ids, &d_ids)).ok()) return s;
+  CK(cudaMemsetAsync(d_ctr, 0, 32 * sizeof(int), st));
+  int* d_act0;
   if (!(s = scratch(a, "act0", ids.size(), &d_act0)).ok()) return s;
-  if (!(s = scratch(a, "act1", ids.size(), &d_act1)).ok()) return s;
-  size_t cap = 0;
-  for (int k : hill_ids) cap = std::max<size_t>(cap, 2 * leaves[k].P);
-  cap = std::max<size_t>(1, cap * hill_ids.size());
-  Work* d_items;
-  if (!(s = scratch(a, "items", 4 * cap, &d_items)).ok()) return s;
-  CK(cudaMemsetAsync(d_ctr, 0, 16 * sizeof(int), st));
   if (!hill_ids.empty()) {
     hpk::k_hill_init<<<((int)ids.size() + T - 1) / T, T, 0, st>>>(b, d_ids, (int)ids.size(),
                                                                    p.uniform_only ? 1 : 0, d_act0,
-                                                                   d_ctr + 8);
+                                                                   d_ctr + 16);
     out.launches++;
   }
-  int n_active = 0;
-  CK(cudaMemcpyAsync(&n_active, d_ctr + 8, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  int iter = 0;
-  while (n_active > 0) {
-    CK(cudaMemsetAsync(d_ctr, 0, 8 * sizeof(int), st));
-    CK(cudaMemsetAsync(d_ctr + 9, 0, sizeof(int), st));
-    hpk::k_gen<<<(n_active + T - 1) / T, T, 0, st>>>(b, d_act0, d_ctr + 8, d_items, (int)cap, d_ctr);
-    out.launches++;
-    for (int cls = 0; cls < 4; ++cls) {
-      launch_eval(cls == 3 ? 8 : cls + 1, b, d_items + (size_t)cls * cap, d_ctr + cls, d_ctr + 4 + cls,
-                  grid, st);
-      out.launches++;
+  std::vector<std::vector<int>> by_cls(hpk::NCLS);
+  std::vector<size_t> items_cls(hpk::NCLS, 0);
+  for (int k : hill_ids) {
+    if (leaves[k].mode != 0) continue;
+    int cls = hpk::eval_class(leaves[k].P, leaves[k].M, gpipe);
+    by_cls[cls].push_back(k);
+    int cpw = hpk::class_cpw(cls, leaves[k].P);
+    items_cls[cls] += (2 * (leaves[k].P - 1) + cpw - 1) / cpw;
+  }
+  size_t qcap = 1024;
+  for (int cls = 0; cls < hpk::NCLS; ++cls) qcap = std::max(qcap, items_cls[cls] + 1024);
+  hpk::AsyncQ q{};
+  if (!(s = scratch(a, "q_slots", qcap, &q.slots)).ok()) return s;
+  if (!(s = scratch(a, "q_seq", qcap, &q.seq)).ok()) return s;
+  unsigned long long* d_q;
+  if (!(s = scratch(a, "q_ctr", 4, &d_q)).ok()) return s;
+  int* d_pending;
+  if (!(s = scratch(a, "q_pending", nL, &d_pending)).ok()) return s;
+  q.head = d_q;
+  q.tail = d_q + 1;
+  q.active = reinterpret_cast<int*>(d_q + 2);
+  q.pending = d_pending;
+  q.cap = qcap;
+  for (int cls = 0; cls < hpk::NCLS; ++cls) {
+    if (by_cls[cls].empty()) continue;
+    int* d_cls_ids;
+    std::string nm = "cls_ids" + std::to_string(cls);
+    if (!(s = upload(a, nm.c_str(), by_cls[cls], &d_cls_ids)).ok()) return s;
+    CK(cudaMemsetAsync(q.seq, 0, sizeof(unsigned long long) * qcap, st));
+    CK(cudaMemsetAsync(d_q, 0, sizeof(unsigned long long) * 4, st));
+    int n = static_cast<int>(by_cls[cls].size());
+    hpk::k_async_seed<<<(n + T - 1) / T, T, 0, st>>>(b, q, d_cls_ids, n, cls);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (a.time_evals) {
+      a.event_pair(&e0, &e1);
+      cudaEventRecord(e0, st);
     }
-    hpk::k_hill_step<<<(n_active + T - 1) / T, T, 0, st>>>(b, d_act0, d_ctr + 8, d_act1, d_ctr + 9);
-    out.launches++;
-    CK(cudaMemcpyAsync(d_ctr + 8, d_ctr + 9, sizeof(int), cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(&n_active, d_ctr + 9, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    std::swap(d_act0, d_act1);
-    ++iter;
+    launch_async(cls, b, q, a.sm_count, st);
+    if (a.time_evals) cudaEventRecord(e1, st);
+    out.launches += 2;
+    out.eval_launches++;
   }
-  out.hill_iterations = iter;
+  out.hill_iterations = 0;
 
   // ---- exhaustive leaves, in chunks of candidates
   if (!exh_ids.empty()) {
@@ -615,7 +1040,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     size_t e = 0;
     long long pos = 0;  // rank position within exh_ids[e]
     while (e < exh_ids.size()) {
-      std::vector<std::vector<Work>> q(4);
+      std::vector<std::vector<Work>> q(hpk::NCLS);
       std::vector<hpk::ExhSpan> spans;
       long long used = 0;
       while (e < exh_ids.size() && used < kChunk) {
@@ -623,9 +1048,8 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
         const Leaf& lf = leaves[k];
         long long total = p.leaves[my_leaves[k]].n_splits;
         long long take = std::min(total - pos, kChunk - used);
-        int K = hpk::k_class(lf.P);
-        int cls = K >= 4 ? 3 : K - 1;
-        int cpw = 32 / hpk::seg_width(lf.P, K);
+        int cls = hpk::eval_class(lf.P, lf.M, gpipe);
+        int cpw = hpk::class_cpw(cls, lf.P);
         for (long long j = 0; j < take; j += cpw)
           q[cls].push_back(Work{k, 2, pos + j, (int)std::min<long long>(cpw, take - j), (int)(used + j)});
         spans.push_back(hpk::ExhSpan{k, (int)used, pos, take});
@@ -660,6 +1084,11 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   CK(cudaStreamSynchronize(st));
   out.simulated = counts[0];
   out.pruned = counts[1];
+  unsigned long long ops = 0;
+  CK(cudaMemcpy(&ops, d_ops, sizeof ops, cudaMemcpyDeviceToHost));
+  out.eval_fp64_ops = static_cast<double>(ops);
+  if (a.time_evals) out.eval_ms = a.drain_events();
+  a.d2h_bytes += sizeof(int) + sizeof counts + sizeof ops;
   out.has_best = best_leaf >= 0;
   if (out.has_best) {
     HillState hs;
@@ -670,7 +1099,10 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
                   cudaMemcpyDeviceToHost));
     out.best_time = hs.best_time;
     out.best_leaf = my_leaves[best_leaf];
+    a.d2h_bytes += sizeof hs + sizeof(int) * lf.P;
   }
+  out.h2d_bytes = a.h2d_bytes;
+  out.d2h_bytes = a.d2h_bytes;
   return hph::Status{};
 }
 
@@ -695,7 +1127,7 @@ hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans
   std::vector<uint8_t> layouts;
   std::vector<int> splits;
   std::vector<double> hop((size_t)n * p.links.size());
-  std::vector<std::vector<Work>> q(4);
+  std::vector<std::vector<Work>> q(hpk::NCLS);
   for (int k = 0; k < n; ++k) {
     const hp_plan& pl = plans[k];
     const int P = pl.n_stages;
@@ -718,8 +1150,7 @@ hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans
       splits.push_back(s.layer_end - s.layer_begin);
       lgs.push_back(hph::leaf_group(p, s.group, s.tp_degree, B, s.dp_degree, s.nodes_used));
     }
-    int K = hpk::k_class(P);
-    q[K >= 4 ? 3 : K - 1].push_back(Work{k, 0, 0, 1, 0});
+    q[hpk::eval_class(P, lf.M, p.schedule == HP_GPIPE)].push_back(Work{k, 0, 0, 1, 0});
   }
   hpk::Bufs b{};
   hph::Status s;
@@ -741,14 +1172,14 @@ hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans
   if (!(s = scratch(a, "e_tseed", 2 * (size_t)n, &b.tseed)).ok()) return s;
   int* d_ctr;
   if (!(s = scratch(a, "e_ctr", 2, &d_ctr)).ok()) return s;
-  for (int cls = 0; cls < 4; ++cls) {
+  for (int cls = 0; cls < hpk::NCLS; ++cls) {
     if (q[cls].empty()) continue;
     Work* d_items;
     std::string nm = "e_q" + std::to_string(cls);
     if (!(s = upload(a, nm.c_str(), q[cls], &d_items)).ok()) return s;
     int cnt[2] = {static_cast<int>(q[cls].size()), 0};
     CK(cudaMemcpyAsync(d_ctr, cnt, sizeof cnt, cudaMemcpyHostToDevice, st));
-    launch_eval(cls == 3 ? 8 : cls + 1, b, d_items, d_ctr, d_ctr + 1, a.sm_count * 8, st);
+    launch_eval(cls, b, d_items, d_ctr, d_ctr + 1, a.sm_count * 8, st);
     CK(cudaStreamSynchronize(st));
   }
   CK(cudaGetLastError());
@@ -760,3 +1191,85 @@ hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans
 }
 
 }  // namespace hpd
+
+// ---------------------------------------------------------------- roofline
+//
+// Microbenchmarks for the FP64 roofline denominator (MEASURED_PEAKS.json has
+// no FP64 figure). k_peak_dadd: 8 independent DADD chains per thread, full
+// occupancy. k_peak_mix: 4 independent copies of the evaluator's node update
+// st = max(a, r); a = st + d; c = max(a, c) + s (4 algorithmic add/max ops).
+namespace hpk {
+
+__global__ void k_peak_dadd(double* out, int iters, double y) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = x[k] + y;
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == -1.0) out[threadIdx.x] = s;
+}
+
+__global__ void k_peak_mix(double* out, int iters, double d, double sd) {
+  double a[4], c[4], r[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    a[k] = threadIdx.x * 1e-9 + k;
+    c[k] = k * 0.5;
+    r[k] = k * 0.25;
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double st = dmax(a[k], r[k]);
+      a[k] = st + d;
+      c[k] = dmax(a[k], c[k]) + sd;
+      r[k] = c[(k + 1) & 3];
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += a[k] + c[k];
+  if (s == -1.0) out[threadIdx.x] = s;
+}
+
+}  // namespace hpk
+
+extern "C" int hp_fp64_peak(int device, double* dadd_ops_per_s, double* mix_ops_per_s) {
+  if (cudaSetDevice(device) != cudaSuccess) return HP_CUDA;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* d_out = nullptr;
+  if (cudaMalloc(&d_out, 1024 * sizeof(double)) != cudaSuccess) return HP_CUDA;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  float best_add = 1e30f, best_mix = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0);
+    hpk::k_peak_dadd<<<blocks, threads>>>(d_out, iters, 1e-12);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep) best_add = ms < best_add ? ms : best_add;
+    cudaEventRecord(e0);
+    hpk::k_peak_mix<<<blocks, threads>>>(d_out, iters, 1e-12, 2e-12);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep) best_mix = ms < best_mix ? ms : best_mix;
+  }
+  double n = (double)blocks * threads * iters;
+  if (dadd_ops_per_s) *dadd_ops_per_s = n * 8 / (best_add * 1e-3);
+  if (mix_ops_per_s) *mix_ops_per_s = n * 16 / (best_mix * 1e-3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d_out);
+  return cudaGetLastError() == cudaSuccess ? HP_OK : HP_CUDA;
+}

@@ -106,6 +106,28 @@ HPD bool cand_less(const Consts& c, double ta, const Leaf& la, const LeafGroup* 
   return enc_less(ea, eb);
 }
 
+// encode_plan order of two splits of the SAME leaf: the strings agree up to
+// the first stage whose layer count differs; there the "end" fields differ
+// and are compared as decimal strings followed by ':' (which sorts after
+// every digit). Equivalent to cand_less for equal (time, pp, leaf).
+HPD bool split_enc_less(int P, const int* a, const int* b) {
+  int s = 0;
+  for (int i = 0; i < P; ++i) {
+    if (a[i] != b[i]) {
+      char da[24], db[24];
+      int na = fmt_ll(s + a[i], da), nb = fmt_ll(s + b[i], db);
+      for (int k = 0;; ++k) {
+        int x = k < na ? (unsigned char)da[k] : ':';
+        int y = k < nb ? (unsigned char)db[k] : ':';
+        if (x != y) return x < y;
+        if (k >= na && k >= nb) return false;
+      }
+    }
+    s += a[i];
+  }
+  return false;
+}
+
 // ------------------------------------------------------------ hill climb
 
 // Per-leaf state of the steepest-descent search (planner.cpp:461-489) plus
@@ -152,8 +174,8 @@ HPD void hill_init(const Consts& c, const Leaf& lf, const LeafGroup* lg, const u
   if (prop_new) {
     if (t_prop >= 0) {
       hs.simulated++;
-      if (!hs.has_best || cand_less(c, t_prop, lf, lg, slots, prop, hs.best_time, lf, lg, slots,
-                                    best_split)) {
+      if (!hs.has_best || t_prop < hs.best_time ||
+          (t_prop == hs.best_time && split_enc_less(P, prop, best_split))) {
         hs.has_best = 1;
         hs.best_time = t_prop;
         for (int i = 0; i < P; ++i) best_split[i] = prop[i];
@@ -258,7 +280,7 @@ HPD void hill_step(const Consts& c, const Leaf& lf, const LeafGroup* lg, const u
         for (int i = 0; i < P; ++i) tmp[i] = cur[i];
         tmp[b] += d;
         tmp[b + 1] -= d;
-        better = cand_less(c, t, lf, lg, slots, tmp, hs.best_time, lf, lg, slots, best_split);
+        better = split_enc_less(P, tmp, best_split);
       }
       if (better) {
         int b = q >> 1, d = (q & 1) ? -1 : 1;

@@ -85,8 +85,8 @@ extern "C" int emu_search(const hp_problem* in, hp_result* res) {
         double tt = eval(c, L, comp.data());
         if (tt >= 0) {
           hs.simulated++;
-          if (!hs.has_best || cand_less(c, tt, L.lf, L.lg.data(), L.slots, comp.data(), hs.best_time,
-                                        L.lf, L.lg.data(), L.slots, bs.data())) {
+          if (!hs.has_best || tt < hs.best_time ||
+              (tt == hs.best_time && split_enc_less(P, comp.data(), bs.data()))) {
             hs.has_best = 1; hs.best_time = tt; bs = comp;
           }
         } else hs.pruned++;

@@ -4,13 +4,20 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle import port
 from paper_2405_16256_b200 import configs, abi, planner
 
-def run(name, cfg, check=True):
+def run(name, cfg, check=True, timed=False):
     P = abi.Problem(cfg)
     eng = planner.engine(0)
-    t0 = time.time(); r = eng.search_shard(P); t1 = time.time()
+    import ctypes as C
+    opts = abi.hp_search_opts(0, 1, 0, abi.HP_FLAG_TIME_KERNELS if timed else 0, 0.0)
+    r = abi.hp_result()
+    t0 = time.time(); st = eng._lib.hp_search(eng._ctx, P.ptr(), C.byref(opts), C.byref(r)); t1 = time.time()
+    assert st == 0, (st, eng._lib.hp_last_error(eng._ctx))
     line = {"cfg": name, "gpu_s": round(t1 - t0, 4), "dev_ms": round(r.device_ms, 2), "sim": r.candidates_simulated,
             "pruned": r.candidates_pruned, "time": r.best_time_s, "launches": r.gpu_launches,
-            "enc": abi.encode_plan(P.group_names, r.best_plan)}
+            "enc": abi.encode_plan(P.group_names, r.best_plan), "iters": r.hill_iterations, "host_ms": round(r.host_ms, 1),
+            "eval_ms": round(r.eval_ms, 2), "eval_launches": r.eval_launches, "fp64_ops": r.eval_fp64_ops,
+            "h2d": r.h2d_bytes, "d2h": r.d2h_bytes}
+    if r.eval_ms > 0: line["eval_tflops"] = round(r.eval_fp64_ops / r.eval_ms / 1e9, 3)
     if check:
         t0 = time.time(); st, o = port.search(P); t1 = time.time()
         line["oracle_s"] = round(t1 - t0, 3)
@@ -32,3 +39,11 @@ if which == "small":
 if which in ("small", "c3"):
     for i in range(2):
         run("C3full", configs.config("C3", full=True), check=False)
+    run("C3full_timed", configs.config("C3", full=True), check=False, timed=True)
+if which in ("small", "peak"):
+    import ctypes as C
+    from paper_2405_16256_b200._lib import lib
+    l = lib(); l.hp_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    a, m = C.c_double(), C.c_double()
+    l.hp_fp64_peak(0, C.byref(a), C.byref(m))
+    print(json.dumps({"fp64_dadd_ops_per_s": a.value, "fp64_mix_ops_per_s": m.value}))
