@@ -1,0 +1,327 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path: the planner's full strategy sweep on C3
+(Llama-140B, 768 devices = 128 AMD + 640 accelerator A).
+
+A "step" is one complete search() over the C3 candidate space
+(time_bound_pruning = false: every leaf's uniform/proportional seeds plus
+its steepest-descent layer-split search, planner.cpp:404-490), ending in the
+exact better_than argmin. value = candidates (simulated + pruned, counted like
+planner.hpp:101-107) per second of device time, inputs resident (CUDA events
+around the device work of each call, max over ranks); e2e = the same through
+the public API (planner.search_sharded -> C ABI) with the problem built from
+host documents and the result read back, every step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1: launched by torchrun, one rank per GPU; ranks take disjoint,
+cost-balanced leaf shards and reduce with one NCCL all-gather (strong
+scaling: the total sweep is fixed). --impl reference times the compiled,
+unmodified reference planner (oracle/_ref) on the host cores, rank 0 only, on a
+bounded deterministic sample of the same sweep.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "candidate plans evaluated/sec (Llama-140B, 768 dev); time-to-optimal-plan"
+UNIT = "candidates/s"
+WORKLOAD = ("C3: Llama-140B (L=160, H=8192, seq 4096) on 768 devices (amd 16x8 + gpu_a 80x8), "
+            "G=1536, B in {1,2}, pp 1..96, full strategy sweep (time_bound_pruning=false)")
+# Deterministic CPU sample of the same sweep (pipeline degrees spread over the
+# range that has feasible candidates); see DESIGN.md "CPU baseline".
+CPU_SAMPLE_PP = [12, 24]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        mx = max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU baseline
+
+def cpu_sample_cfg():
+    from paper_2405_16256_b200 import configs
+    return configs.with_pp(configs.config("C3", full=True), CPU_SAMPLE_PP)
+
+
+def run_reference_once(cfg, jobs):
+    """The compiled, unmodified reference search() (oracle/_ref), or the C port
+    when the reference library is absent. Returns (candidates, seconds, kind)."""
+    from oracle import ref
+    if ref.available():
+        r = ref.search(cfg, jobs=jobs)
+        if r.get("status") != 0:
+            raise RuntimeError(f"reference search failed: {r.get('error')}")
+        return r["candidates_simulated"] + r["candidates_pruned"], r["wall_s"], "reference"
+    from oracle import port
+    from paper_2405_16256_b200 import abi
+    p = abi.Problem(cfg)
+    t0 = time.perf_counter()
+    st, res = port.search(p)
+    return res.candidates_simulated + res.candidates_pruned, time.perf_counter() - t0, "port"
+
+
+def cpu_baseline(jobs):
+    cfg = cpu_sample_cfg()
+    cands, secs, kind = run_reference_once(cfg, jobs)
+    return {"value": cands / secs, "unit": UNIT, "cores": jobs if kind == "reference" else 1, "kind": kind,
+            "sample": f"C3 full sweep restricted to pipeline degrees {CPU_SAMPLE_PP} ({cands} candidates, "
+                      f"{secs:.2f} s)"}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------ reference arm
+
+def main_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    jobs = os.cpu_count() or 1
+    cfg = cpu_sample_cfg()
+    for _ in range(args.warmup):
+        run_reference_once(cfg, jobs)
+    vals, secs_all, kind, cands = [], [], None, 0
+    for _ in range(args.steps):
+        cands, secs, kind = run_reference_once(cfg, jobs)
+        vals.append(cands / secs)
+        secs_all.append(secs)
+    ms = sum(secs_all) / len(secs_all) * 1e3
+    value = cands / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOAD, "sample_pipeline_degrees": CPU_SAMPLE_PP,
+                       "candidates_per_step": cands, "cpu": cpu_model(), "threads": jobs},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": jobs if kind == "reference" else 1,
+                             "kind": kind, "sample": f"C3 full sweep, pipeline degrees {CPU_SAMPLE_PP}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+
+def main_ours(args):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_16256_b200 import abi, configs, planner
+    from paper_2405_16256_b200._lib import lib
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one rank per GPU)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    docs = configs.config(args.config, full=True)
+    eng = planner.engine(local)
+    problem = abi.Problem(docs)
+
+    def one_step(flags=0):
+        """One full search through the public path: host documents -> C ABI
+        -> sm_100a kernels -> per-rank result -> NCCL all-gather -> exact
+        reduction. Returns (reduced, mine)."""
+        p = abi.Problem(docs)
+        opts = abi.hp_search_opts(rank, world, 0, flags, 0.0)
+        mine = abi.hp_result()
+        st = eng._lib.hp_search(eng._ctx, p.ptr(), C.byref(opts), C.byref(mine))
+        if st != abi.HP_OK:
+            raise RuntimeError(eng._lib.hp_last_error(eng._ctx).decode())
+        if world == 1:
+            return mine, mine
+        nbytes = C.sizeof(abi.hp_result)
+        t = torch.frombuffer(bytearray(C.string_at(C.byref(mine), nbytes)), dtype=torch.uint8).cuda()
+        g = torch.empty(world * nbytes, dtype=torch.uint8, device="cuda")
+        dist.all_gather_into_tensor(g, t)
+        host = g.cpu().numpy().tobytes()
+        recs = []
+        for r in range(world):
+            rec = abi.hp_result()
+            C.memmove(C.byref(rec), host[r * nbytes:(r + 1) * nbytes], nbytes)
+            recs.append(rec)
+        return planner.reduce_results(p, recs), mine
+
+    # L2 flush buffer (> 126 MB L2) written between timed steps
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+
+    dev_ms, wall_ms, eval_ms, eval_ops, launches, h2d, d2h = [], [], 0.0, 0.0, 0, 0.0, 0.0
+    red = None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            red, mine = one_step(abi.HP_FLAG_TIME_KERNELS)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            if world > 1:
+                dist.barrier()
+            dev_ms.append(mine.device_ms)
+            wall_ms.append((t1 - t0) * 1e3)
+            eval_ms += mine.eval_ms
+            eval_ops += mine.eval_fp64_ops
+            launches = mine.gpu_launches
+            h2d, d2h = mine.h2d_bytes, mine.d2h_bytes
+    torch.cuda.synchronize()
+
+    # max over ranks of the per-step times; sums of bytes/launches over ranks
+    vec = torch.tensor([sum(dev_ms) / len(dev_ms), sum(wall_ms) / len(wall_ms)], dtype=torch.float64,
+                       device="cuda")
+    agg = torch.tensor([h2d, d2h, float(launches), eval_ms, eval_ops], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+        dist.all_reduce(agg, op=dist.ReduceOp.SUM)
+    dev_step_ms, wall_step_ms = float(vec[0]), float(vec[1])
+    h2d, d2h, launches, eval_ms_all, eval_ops_all = [float(x) for x in agg]
+
+    cands = red.candidates_simulated + red.candidates_pruned
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    l = lib()
+    l.hp_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    dadd, mix = C.c_double(), C.c_double()
+    l.hp_fp64_peak(local, C.byref(dadd), C.byref(mix))
+    achieved = eval_ops_all / (eval_ms_all * 1e-3) if eval_ms_all > 0 else None
+    peak = dadd.value
+    traffic = None
+    tf = os.path.join(HERE, "profiles", "latest_eval_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": cands / (dev_step_ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_step_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "time_to_plan_s": wall_step_ms / 1e3,
+        "config": {"workload": WORKLOAD, "candidates_per_step": cands,
+                   "candidates_simulated": red.candidates_simulated, "candidates_pruned": red.candidates_pruned,
+                   "best_iteration_time_s": red.best_time_s,
+                   "best_plan": abi.encode_plan(problem.group_names, red.best_plan),
+                   "parallelism": f"leaf-sharded x{world}",
+                   "l2": "flushed between timed steps (256 MiB write); per-step inputs are KB-sized tables"},
+        "e2e": {"value": cands / (wall_step_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "fp64", "achieved": achieved / 1e12 if achieved else None,
+                     "peak": peak / 1e12, "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+                     "traffic": traffic,
+                     "note": ("algorithmic FP64 add+max ops of the evaluator kernels (8PM-4M per simulated "
+                              "candidate) / their CUDA-event time; peak = measured DADD rate on this GPU "
+                              f"({peak / 1e12:.2f} T/s); the add/max node-update mix peaks at "
+                              f"{mix.value / 1e12:.2f} T/s on the same GPU")},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline(os.cpu_count() or 1)
+            cb["cpu"] = cpu_model()
+            line["cpu_baseline"] = cb
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return main_reference(args)
+    return main_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
