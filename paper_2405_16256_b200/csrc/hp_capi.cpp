@@ -82,10 +82,22 @@ hp_status hp_validate(hp_ctx* ctx, const hp_problem* problem) {
 
 hp_status hp_probe(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts* opts,
                    double* bound) {
-  (void)opts;
-  (void)problem;
-  if (bound) *bound = std::numeric_limits<double>::infinity();
-  return fail(ctx, HP_INTERNAL, "hp_probe: default (pruned) mode not built yet");
+  if (!ctx || !bound) return HP_INTERNAL;
+  cudaSetDevice(ctx->arena.device);
+  *bound = std::numeric_limits<double>::infinity();
+  hph::Problem p;
+  hp_status st = prepare(ctx, problem, p);
+  if (st != HP_OK) return st;
+  int shard = opts ? opts->shard_index : 0;
+  int nshard = opts && opts->shard_count > 0 ? opts->shard_count : 1;
+  if (shard < 0 || shard >= nshard) return fail(ctx, HP_BAD_CONFIG, "bad shard index");
+  if (!p.pruning) return HP_OK;  // no probe pass when pruning is off
+  hpd::SearchOut out;
+  hph::Status s = hpd::search_default(ctx->arena, p, hph::shard_tasks(p, shard, nshard), false, 0.0,
+                                      true, out);
+  if (!s.ok()) return fail(ctx, s);
+  *bound = out.global_bound;
+  return HP_OK;
 }
 
 hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts* opts,
@@ -100,9 +112,11 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   int shard = opts ? opts->shard_index : 0;
   int nshard = opts && opts->shard_count > 0 ? opts->shard_count : 1;
   if (shard < 0 || shard >= nshard) return fail(ctx, HP_BAD_CONFIG, "bad shard index");
+  if (nshard > 1 && p.pruning && !(opts && opts->have_global_bound))
+    return fail(ctx, HP_BAD_CONFIG,
+                "sharded default-mode search needs the all-shard probe bound (hp_probe)");
   result->tasks = static_cast<int64_t>(p.tasks.size());
   result->global_bound = std::numeric_limits<double>::infinity();
-  if (p.pruning) return fail(ctx, HP_INTERNAL, "default (pruned) mode not built yet");
 
   // Task-level prunes (planner.cpp:317-327, 395-400) are host decisions;
   // shard 0 reports them.
@@ -117,12 +131,20 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
       }
     }
   }
-  std::vector<int> mine = hph::shard_leaves(p, shard, nshard);
+  std::vector<int> mine;
+  if (p.pruning) mine = hph::shard_tasks(p, shard, nshard);
+  else mine = hph::shard_leaves(p, shard, nshard);
   result->host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
   ctx->arena.time_evals = opts && (opts->flags & HP_FLAG_TIME_KERNELS);
   hpd::SearchOut out;
   cudaEventRecord(ctx->ev0, ctx->arena.stream);
-  hph::Status s = hpd::search_full(ctx->arena, p, mine, out);
+  hph::Status s;
+  if (p.pruning) {
+    bool have = opts && opts->have_global_bound;
+    s = hpd::search_default(ctx->arena, p, mine, have, have ? opts->global_bound : 0.0, false, out);
+  } else {
+    s = hpd::search_full(ctx->arena, p, mine, out);
+  }
   if (!s.ok()) return fail(ctx, s);
   cudaEventRecord(ctx->ev1, ctx->arena.stream);
   cudaEventSynchronize(ctx->ev1);
@@ -136,10 +158,22 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   result->h2d_bytes = out.h2d_bytes;
   result->d2h_bytes = out.d2h_bytes + sizeof(hp_result);
   result->hill_iterations = out.hill_iterations;
-  result->leaves = static_cast<int64_t>(mine.size());
+  result->global_bound = p.pruning ? out.global_bound : std::numeric_limits<double>::infinity();
+  if (p.pruning) {
+    long long nl = 0;
+    for (int ti : mine) nl += p.tasks[ti].leaf_end - p.tasks[ti].leaf_begin;
+    result->leaves = nl;
+  } else {
+    result->leaves = static_cast<int64_t>(mine.size());
+  }
   result->candidates_simulated += out.simulated;
   result->candidates_pruned += out.pruned;
-  result->reason_counts[HP_REASON_MEMORY] += out.pruned;
+  if (p.pruning) {
+    result->reason_counts[HP_REASON_MEMORY] += out.pruned_mem;
+    result->reason_counts[HP_REASON_BOUND] += out.pruned_bound;
+  } else {
+    result->reason_counts[HP_REASON_MEMORY] += out.pruned;
+  }
   if (out.has_best) {
     result->has_best = 1;
     result->best_time_s = out.best_time;

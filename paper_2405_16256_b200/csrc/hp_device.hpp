@@ -71,7 +71,7 @@ struct Arena {
 };
 
 struct SearchOut {
-  long long simulated = 0, pruned = 0;
+  long long simulated = 0, pruned = 0, pruned_mem = 0, pruned_bound = 0;
   bool has_best = false;
   double best_time = 0.0;
   int best_leaf = -1;          // index into Problem::leaves
@@ -88,6 +88,12 @@ struct SearchOut {
 // Full strategy sweep (time_bound_pruning = false) over `my_leaves`.
 hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>& my_leaves,
                         SearchOut& out);
+
+// Time-bound-pruned (default) mode over whole tasks; runs the probe pass
+// first unless have_bound (then `bound` is the all-shard probe minimum).
+// probe_only stops after the probe (out.global_bound = this shard's min).
+hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<int>& my_tasks,
+                           bool have_bound, double bound, bool probe_only, SearchOut& out);
 
 // Batched evaluate_plan_unchecked(...).sim.iteration_time_s of explicit plans.
 hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans, int n,

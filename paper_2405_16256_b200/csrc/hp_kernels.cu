@@ -16,9 +16,13 @@
 //                  one leaf, lane = K consecutive pipeline stages; the 1F1B /
 //                  GPipe DAG runs level-synchronously with __shfl exchange of
 //                  the neighbours' channel state (hp_core.cuh).
-//   k_hill_init / k_gen / k_hill_step
+//   k_hill_init / k_async_seed / k_hill_async
 //                  steepest-descent layer-split search (planner.cpp:461-489)
-//                  with memo-equivalent counting (hp_search_core.cuh).
+//                  with memo-equivalent counting (hp_search_core.cuh); every
+//                  leaf advances independently through a device work queue.
+//   k_default      time-bound-pruned (default) mode: one warp per task,
+//                  speculative batch evaluation + in-order replay of the
+//                  incumbent (planner.cpp:519-534).
 //   k_exh_reduce   per-leaf reduction of exhaustively enumerated splits.
 //   k_final        exact better_than argmin over leaf bests.
 #include <cuda_runtime.h>
@@ -26,6 +30,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -50,7 +55,12 @@ struct Work {
   long long first;
   int n;
   int out;
+  const long long* ids;  // optional: candidate s is ids[first + s]
 };
+
+__device__ __forceinline__ long long cand_id(const Work& w, int s) {
+  return w.ids ? w.ids[w.first + s] : w.first + s;
+}
 
 struct Bufs {
   const Leaf* leaves;
@@ -147,9 +157,9 @@ __global__ void k_seeds(Bufs b, int n_leaves) {
 // for exhaustive items is done per lane for its own stages).
 __device__ __forceinline__ int cand_count(const Bufs& b, const Leaf& lf, const Work& w, int s,
                                           int i) {
-  if (w.kind == 0) return (w.first + s == 0 ? b.uni : b.prop)[lf.split_off + i];
+  if (w.kind == 0) return (cand_id(w, s) == 0 ? b.uni : b.prop)[lf.split_off + i];
   if (w.kind == 1) {
-    int q = (int)w.first + s;
+    int q = (int)cand_id(w, s);
     int mb = q >> 1, d = (q & 1) ? -1 : 1;
     int c = __ldcg(b.cur + lf.split_off + i);  // written by another SM's hill step
     if (i == mb) c += d;
@@ -181,7 +191,7 @@ __device__ __forceinline__ void eval_item_generic(const Bufs& b, const Work& w, 
     int cnt[K];
     if (w.kind == 2 && has_cand) {
       // unrank this candidate's composition up to my last stage
-      long long rank = w.first + seg;
+      long long rank = cand_id(w, seg);
       int rem = c_consts.L;
       int last = min(P - 1, sl * K + K - 1);
       for (int j = 0; j <= last; ++j) {
@@ -274,8 +284,8 @@ __device__ __forceinline__ void eval_item_generic(const Bufs& b, const Work& w, 
     for (int off = W2 >> 1; off > 0; off >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, off));
     if (sl == 0 && has_cand) {
       double t = inv ? T_INVALID : (mem ? T_MEMORY : v);
-      if (w.kind == 0) b.tseed[2 * w.leaf + (int)w.first + seg] = t;
-      else if (w.kind == 1) b.nb[b.nb_off[w.leaf] + (int)w.first + seg] = t;
+      if (w.kind == 0) b.tseed[2 * w.leaf + (int)cand_id(w, seg)] = t;
+      else if (w.kind == 1) b.nb[b.nb_off[w.leaf] + (int)cand_id(w, seg)] = t;
       else b.xbuf[w.out + seg] = t;
       if (run && b.ops) atomicAdd(b.ops, (unsigned long long)(8LL * P * M - 4LL * M));
     }
@@ -310,7 +320,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
   bool valid = true, mem_ok = true;
   int cnt[K];
   if (w.kind == 2 && has_cand) {
-    long long rank = w.first + seg;
+    long long rank = cand_id(w, seg);
     int rem = c_consts.L;
     int last = min(P - 1, sl * K + K - 1);
     for (int j = 0; j <= last; ++j) {
@@ -473,8 +483,8 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
   }
   if (sl == 0 && has_cand) {
     double tt = inv ? T_INVALID : (mem ? T_MEMORY : v);
-    if (w.kind == 0) b.tseed[2 * w.leaf + (int)w.first + seg] = tt;
-    else if (w.kind == 1) b.nb[b.nb_off[w.leaf] + (int)w.first + seg] = tt;
+    if (w.kind == 0) b.tseed[2 * w.leaf + (int)cand_id(w, seg)] = tt;
+    else if (w.kind == 1) b.nb[b.nb_off[w.leaf] + (int)cand_id(w, seg)] = tt;
     else b.xbuf[w.out + seg] = tt;
     if (run && b.ops) atomicAdd(b.ops, (unsigned long long)(8LL * P * M - 4LL * M));
   }
@@ -532,6 +542,7 @@ __device__ void push_items(const Bufs& b, const AsyncQ& q, int li, int cls) {
     w.first = j * cpw;
     w.n = min(cpw, nslots - j * cpw);
     w.out = 0;
+    w.ids = nullptr;
     const unsigned long long k = (t + j) % q.cap;
     q.slots[k] = w;
     __threadfence();
@@ -585,6 +596,7 @@ __global__ void __launch_bounds__(256) k_hill_async(Bufs b, AsyncQ q, int cls) {
     w.first = __shfl_sync(0xffffffffu, w.first, 0);
     w.n = __shfl_sync(0xffffffffu, w.n, 0);
     w.out = 0;
+    w.ids = nullptr;
     eval_item<K, FAST>(b, w, lane);
     __syncwarp();
     if (lane == 0) {
@@ -627,48 +639,6 @@ __global__ void k_hill_init(Bufs b, const int* leaf_ids, int n, int uniform_only
             b.cur + lf.split_off, b.best + lf.split_off, hs, uniform_only != 0);
   b.hs[li] = hs;
   if (hs.active) active[atomicAdd(n_active, 1)] = li;
-}
-
-// Work items for the neighbours of every active leaf, bucketed by K class.
-__global__ void k_gen(Bufs b, const int* active, const int* n_active, Work* items, int cap,
-                      int* n_items /*[NCLS]*/) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= *n_active) return;
-  int li = active[k];
-  const Leaf lf = b.leaves[li];
-  int cls = eval_class(lf.P, lf.M, c_consts.schedule == 0);
-  int cpw = class_cpw(cls, lf.P);
-  int nslots = 2 * (lf.P - 1);
-  int nit = (nslots + cpw - 1) / cpw;
-  int base = atomicAdd(&n_items[cls], nit);
-  Work* q = items + (size_t)cls * cap;
-  for (int j = 0; j < nit; ++j) {
-    Work w;
-    w.leaf = li;
-    w.kind = 1;
-    w.first = j * cpw;
-    w.n = min(cpw, nslots - j * cpw);
-    w.out = 0;
-    q[base + j] = w;
-  }
-}
-
-__global__ void k_hill_step(Bufs b, const int* active, const int* n_active, int* next_active,
-                            int* n_next) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= *n_active) return;
-  int li = active[k];
-  const Leaf lf = b.leaves[li];
-  HillState hs = b.hs[li];
-  int delta[HP_MAX_STAGES];
-  unsigned char old[2 * HP_MAX_STAGES];
-  int tmp[HP_MAX_STAGES];
-  for (int i = 0; i < lf.P; ++i) delta[i] = 0;
-  hill_step(c_consts, lf, b.lg + lf.lg_off, b.layouts + lf.layout_off, b.cur + lf.split_off,
-            b.uni + lf.split_off, b.prop + lf.split_off, b.best + lf.split_off,
-            b.hist + b.hist_off[li], hs, b.nb + b.nb_off[li], delta, old, tmp);
-  b.hs[li] = hs;
-  if (hs.active) next_active[atomicAdd(n_next, 1)] = li;
 }
 
 // ------------------------------------------------------------------ exhaustive
@@ -767,6 +737,52 @@ __global__ void k_final(Bufs b, int n_leaves, int* out_leaf, long long* counts) 
   }
 }
 
+#include "hp_default.cuh"
+
+// Exact argmin over per-task bests of the default mode (one block).
+__global__ void k_final_tasks(Bufs b, const TaskRes* res, const TaskDev* tasks, const int* tbest_rows,
+                              int n, int* out_task, long long* counts) {
+  __shared__ int s_best[1024];
+  __shared__ long long s_c[3][1024];
+  const int tid = threadIdx.x;
+  int mine = -1;
+  long long c0 = 0, c1 = 0, c2 = 0;
+  auto less = [&](int x, int y) {
+    const TaskRes& rx = res[x];
+    const TaskRes& ry = res[y];
+    const Leaf lx = b.leaves[rx.best_leaf], ly = b.leaves[ry.best_leaf];
+    return cand_less(c_consts, rx.best_time, lx, b.lg + lx.lg_off, b.layouts + lx.layout_off,
+                     tbest_rows + tasks[x].best_off, ry.best_time, ly, b.lg + ly.lg_off,
+                     b.layouts + ly.layout_off, tbest_rows + tasks[y].best_off);
+  };
+  for (int k = tid; k < n; k += blockDim.x) {
+    c0 += res[k].simulated;
+    c1 += res[k].pruned_mem;
+    c2 += res[k].pruned_bound;
+    if (!res[k].has_best) continue;
+    if (mine < 0 || less(k, mine)) mine = k;
+  }
+  s_best[tid] = mine;
+  s_c[0][tid] = c0;
+  s_c[1][tid] = c1;
+  s_c[2][tid] = c2;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (tid < st) {
+      int x = s_best[tid], y = s_best[tid + st];
+      if (y >= 0 && (x < 0 || less(y, x))) s_best[tid] = y;
+      for (int q = 0; q < 3; ++q) s_c[q][tid] += s_c[q][tid + st];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *out_task = s_best[0];
+    counts[0] = s_c[0][0];
+    counts[1] = s_c[1][0];
+    counts[2] = s_c[2][0];
+  }
+}
+
 }  // namespace hpk
 
 // ====================================================================== host
@@ -838,8 +854,11 @@ static void launch_async(int cls, const hpk::Bufs& b, const hpk::AsyncQ& q, int 
   }
 }
 
-hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>& my_leaves,
-                        SearchOut& out) {
+// Split-independent tables of `my_leaves` (host, exact reference order),
+// uploaded with the per-leaf device state buffers.
+static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vector<int>& my_leaves,
+                                hpk::Bufs& b, std::vector<Leaf>& leaves, std::vector<int>& hill_ids,
+                                std::vector<int>& exh_ids) {
   cudaStream_t st = a.stream;
   const int G = static_cast<int>(p.groups.size());
   const int nL = static_cast<int>(my_leaves.size());
@@ -850,7 +869,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   a.d2h_bytes = 0;
 
   // ---- host tables (split-independent, exact reference order)
-  std::vector<Leaf> leaves(nL);
+  leaves.assign(nL, Leaf{});
   std::vector<LeafGroup> lgs((size_t)nL * G);
   std::vector<int> hist_off(nL), nb_off(nL);
   std::vector<double> hop(p.mbs.size() * p.links.size());
@@ -858,7 +877,8 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     for (size_t l = 0; l < p.links.size(); ++l)
       hop[bi * p.links.size() + l] = hph::hop_time(p, (int)l, p.mbs[bi]);
   int split_total = 0, hist_total = 0, nb_total = 0;
-  std::vector<int> hill_ids, exh_ids;
+  hill_ids.clear();
+  exh_ids.clear();
   for (int k = 0; k < nL; ++k) {
     const hph::LeafHost& h = p.leaves[my_leaves[k]];
     const hph::Task& t = p.tasks[h.task];
@@ -886,7 +906,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     else hill_ids.push_back(k);
   }
 
-  hpk::Bufs b{};
+  b = hpk::Bufs{};
   hph::Status s;
   Leaf* d_leaves;
   LeafGroup* d_lg;
@@ -914,6 +934,18 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   if (!(s = scratch(a, "nb", nb_total, &b.nb)).ok()) return s;
   if (!(s = scratch(a, "hs", nL, &b.hs)).ok()) return s;
   CK(cudaMemsetAsync(b.hs, 0, sizeof(HillState) * std::max(1, nL), st));
+  return hph::Status{};
+}
+
+hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>& my_leaves,
+                        SearchOut& out) {
+  cudaStream_t st = a.stream;
+  const int nL = static_cast<int>(my_leaves.size());
+  hpk::Bufs b;
+  std::vector<Leaf> leaves;
+  std::vector<int> hill_ids, exh_ids;
+  hph::Status s = setup_tables(a, p, my_leaves, b, leaves, hill_ids, exh_ids);
+  if (!s.ok()) return s;
 
   // counters: [0..7] items per class, [8..15] next-item per class,
   // [16] n_active, [17] n_next, [18..19] one-off queue count / next
@@ -952,10 +984,10 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     int cpw = hpk::class_cpw(cls, leaves[k].P);
     int n = p.uniform_only ? 1 : 2;
     if (cpw >= n) {
-      seedq[cls].push_back(Work{k, 0, 0, n, 0});
+      seedq[cls].push_back(Work{k, 0, 0, n, 0, nullptr});
     } else {
-      seedq[cls].push_back(Work{k, 0, 0, 1, 0});
-      if (n == 2) seedq[cls].push_back(Work{k, 0, 1, 1, 0});
+      seedq[cls].push_back(Work{k, 0, 0, 1, 0, nullptr});
+      if (n == 2) seedq[cls].push_back(Work{k, 0, 1, 1, 0, nullptr});
     }
   }
   auto run_queues = [&](std::vector<std::vector<Work>>& qs, const char* tag) -> hph::Status {
@@ -1051,7 +1083,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
         int cls = hpk::eval_class(lf.P, lf.M, gpipe);
         int cpw = hpk::class_cpw(cls, lf.P);
         for (long long j = 0; j < take; j += cpw)
-          q[cls].push_back(Work{k, 2, pos + j, (int)std::min<long long>(cpw, take - j), (int)(used + j)});
+          q[cls].push_back(Work{k, 2, pos + j, (int)std::min<long long>(cpw, take - j), (int)(used + j), nullptr});
         spans.push_back(hpk::ExhSpan{k, (int)used, pos, take});
         used += take;
         pos += take;
@@ -1150,7 +1182,7 @@ hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans
       splits.push_back(s.layer_end - s.layer_begin);
       lgs.push_back(hph::leaf_group(p, s.group, s.tp_degree, B, s.dp_degree, s.nodes_used));
     }
-    q[hpk::eval_class(P, lf.M, p.schedule == HP_GPIPE)].push_back(Work{k, 0, 0, 1, 0});
+    q[hpk::eval_class(P, lf.M, p.schedule == HP_GPIPE)].push_back(Work{k, 0, 0, 1, 0, nullptr});
   }
   hpk::Bufs b{};
   hph::Status s;
@@ -1273,3 +1305,123 @@ extern "C" int hp_fp64_peak(int device, double* dadd_ops_per_s, double* mix_ops_
   cudaFree(d_out);
   return cudaGetLastError() == cudaSuccess ? HP_OK : HP_CUDA;
 }
+
+namespace hpd {
+
+// Default (time-bound-pruned) mode over whole tasks `my_tasks` (reference
+// order). When !have_bound the probe pass runs first (planner.cpp:640-651)
+// over the same tasks; its min is the global bound (a sharded caller passes
+// the all-reduced min instead).
+hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<int>& my_tasks,
+                           bool have_bound, double bound, bool probe_only, SearchOut& out) {
+  cudaStream_t st = a.stream;
+  std::vector<int> my_leaves;
+  std::vector<hpk::TaskDev> tasks;
+  int best_total = 0;
+  for (int ti : my_tasks) {
+    const hph::Task& t = p.tasks[ti];
+    hpk::TaskDev td;
+    td.leaf_begin = static_cast<int>(my_leaves.size());
+    for (int li = t.leaf_begin; li < t.leaf_end; ++li) my_leaves.push_back(li);
+    td.leaf_end = static_cast<int>(my_leaves.size());
+    td.pp = t.pp;
+    td.best_off = best_total;
+    best_total += t.pp;
+    if (td.leaf_end > td.leaf_begin) tasks.push_back(td);
+  }
+  hpk::Bufs b;
+  std::vector<Leaf> leaves;
+  std::vector<int> hill_ids, exh_ids;
+  hph::Status s = setup_tables(a, p, my_leaves, b, leaves, hill_ids, exh_ids);
+  if (!s.ok()) return s;
+  const int nT = static_cast<int>(tasks.size());
+  out.global_bound = have_bound ? bound : std::numeric_limits<double>::infinity();
+  if (nT == 0) return hph::Status{};
+  hpk::TaskDev* d_tasks;
+  if (!(s = upload(a, "d_tasks", tasks, &d_tasks)).ok()) return s;
+  hpk::TaskRes* d_res;
+  int* d_tbest;
+  if (!(s = scratch(a, "d_tres", nT, &d_res)).ok()) return s;
+  if (!(s = scratch(a, "d_tbest", best_total, &d_tbest)).ok()) return s;
+  const int threads = 128;
+  const int warps = std::min(nT, a.sm_count * 16);
+  const int blocks = (warps * 32 + threads - 1) / threads;
+  const size_t nw = (size_t)blocks * (threads / 32);
+  hpk::DefScratch sc;
+  sc.CH = hpk::DEF_CH;
+  if (!(s = scratch(a, "sc_ids", nw * sc.CH, &sc.ids)).ok()) return s;
+  if (!(s = scratch(a, "sc_lower", nw * sc.CH, &sc.lower)).ok()) return s;
+  if (!(s = scratch(a, "sc_times", nw * sc.CH, &sc.times)).ok()) return s;
+  if (!(s = scratch(a, "sc_flag", nw * sc.CH, &sc.flag)).ok()) return s;
+  if (!(s = scratch(a, "sc_dec", nw * sc.CH, &sc.dec)).ok()) return s;
+  int* d_next;
+  if (!(s = scratch(a, "d_next", 4, &d_next)).ok()) return s;
+  unsigned long long* d_ops;
+  if (!(s = scratch(a, "ops", 1, &d_ops)).ok()) return s;
+  CK(cudaMemsetAsync(d_ops, 0, sizeof(unsigned long long), st));
+  b.ops = d_ops;
+
+  if (!have_bound) {
+    CK(cudaMemsetAsync(d_next, 0, sizeof(int), st));
+    hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, nT, d_next, d_res, d_tbest, sc, 0.0, 1,
+                                               p.uniform_only ? 1 : 0);
+    out.launches++;
+    out.eval_launches++;
+    std::vector<hpk::TaskRes> pr(nT);
+    CK(cudaMemcpyAsync(pr.data(), d_res, sizeof(hpk::TaskRes) * nT, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    a.d2h_bytes += sizeof(hpk::TaskRes) * nT;
+    double gb = std::numeric_limits<double>::infinity();
+    for (const auto& r : pr) gb = std::min(gb, r.probe_time);
+    out.global_bound = gb;
+    if (probe_only) return hph::Status{};
+  }
+  CK(cudaMemsetAsync(d_next, 0, sizeof(int), st));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (a.time_evals) {
+    a.event_pair(&e0, &e1);
+    cudaEventRecord(e0, st);
+  }
+  hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, nT, d_next, d_res, d_tbest, sc,
+                                             out.global_bound, 0, p.uniform_only ? 1 : 0);
+  if (a.time_evals) cudaEventRecord(e1, st);
+  out.launches++;
+  out.eval_launches++;
+  int* d_bt;
+  long long* d_counts;
+  if (!(s = scratch(a, "d_bt", 1, &d_bt)).ok()) return s;
+  if (!(s = scratch(a, "d_counts3", 3, &d_counts)).ok()) return s;
+  hpk::k_final_tasks<<<1, 1024, 0, st>>>(b, d_res, d_tasks, d_tbest, nT, d_bt, d_counts);
+  out.launches++;
+  CK(cudaGetLastError());
+  int bt = -1;
+  long long counts[3];
+  unsigned long long ops = 0;
+  CK(cudaMemcpyAsync(&bt, d_bt, sizeof bt, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(counts, d_counts, sizeof counts, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&ops, d_ops, sizeof ops, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (a.time_evals) out.eval_ms = a.drain_events();
+  out.eval_fp64_ops = static_cast<double>(ops);
+  out.simulated = counts[0];
+  out.pruned = counts[1] + counts[2];
+  out.pruned_mem = counts[1];
+  out.pruned_bound = counts[2];
+  out.has_best = bt >= 0;
+  if (out.has_best) {
+    hpk::TaskRes r;
+    CK(cudaMemcpy(&r, d_res + bt, sizeof r, cudaMemcpyDeviceToHost));
+    out.best_time = r.best_time;
+    out.best_leaf = my_leaves[r.best_leaf];
+    out.best_split.resize(tasks[bt].pp);
+    CK(cudaMemcpy(out.best_split.data(), d_tbest + tasks[bt].best_off, sizeof(int) * tasks[bt].pp,
+                  cudaMemcpyDeviceToHost));
+    a.d2h_bytes += sizeof r + sizeof(int) * tasks[bt].pp;
+  }
+  a.d2h_bytes += sizeof bt + sizeof counts + sizeof ops;
+  out.h2d_bytes = a.h2d_bytes;
+  out.d2h_bytes = a.d2h_bytes;
+  return hph::Status{};
+}
+
+}  // namespace hpd

@@ -47,3 +47,22 @@ if which in ("small", "peak"):
     a, m = C.c_double(), C.c_double()
     l.hp_fp64_peak(0, C.byref(a), C.byref(m))
     print(json.dumps({"fp64_dadd_ops_per_s": a.value, "fp64_mix_ops_per_s": m.value}))
+if which in ("default",):
+    from oracle import ref
+    for n in ["C0", "C1", "C2u", "C2", "C3"]:
+        cfg = configs.config(n, full=False)
+        P = abi.Problem(cfg)
+        eng = planner.engine(0)
+        t0 = time.time(); r = eng.search_shard(P); t1 = time.time()
+        rr = ref.search(cfg, jobs=os.cpu_count())
+        enc = abi.encode_plan(P.group_names, r.best_plan)
+        renc = abi.encode_plan(P.group_names, P.plan_from_doc(rr["plan"]))
+        line = {"cfg": n + "-default", "gpu_s": round(t1 - t0, 4), "dev_ms": round(r.device_ms, 2),
+                "sim": r.candidates_simulated, "pruned": r.candidates_pruned, "time": r.best_time_s,
+                "gb": r.global_bound, "ref_s": rr["wall_s"],
+                "match": (rr["candidates_simulated"] == r.candidates_simulated and
+                          rr["candidates_pruned"] == r.candidates_pruned and
+                          rr["eval"]["iteration_time_s"] == r.best_time_s and renc == enc)}
+        if not line["match"]:
+            line["ref"] = [rr["candidates_simulated"], rr["candidates_pruned"], rr["eval"]["iteration_time_s"], renc, enc]
+        print(json.dumps(line), flush=True)
