@@ -207,7 +207,8 @@ const char* hp_last_error(const hp_ctx* ctx);
 int hp_abi_version(void);
 
 /* Validation of the specs (types.cpp:78-163) and planner config
- * (planner.cpp:600-607). Host only. */
+ * (planner.cpp:600-607). Host only; ctx may be NULL (then hp_last_error(NULL)
+ * returns this thread's last message). */
 hp_status hp_validate(hp_ctx* ctx, const hp_problem* problem);
 
 /* Probe pass for this shard (planner.cpp:640-651): min over the shard's tasks

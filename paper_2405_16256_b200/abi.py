@@ -161,7 +161,9 @@ class Problem:
             G.devices_per_node = int(_req(g, "devices_per_node", "cluster.group"))
             G.compute_efficiency = float(g.get("compute_efficiency", 1.0))
             G.bwd_fwd_ratio = float(g.get("bwd_fwd_ratio", 2.0))
-        idx = {n: i for i, n in enumerate(self.group_names)}
+        idx = {}
+        for i, n in enumerate(self.group_names):
+            idx.setdefault(n, i)
         self._links = (hp_link * max(1, len(links)))()
         for i, l in enumerate(links):
             ep = l.get("endpoints", l)
@@ -170,16 +172,16 @@ class Problem:
                 raise ConfigError(f"cluster.link: unknown link kind '{kind}'")
             L = self._links[i]
             L.scope = _SCOPES[kind]
+            # Unknown names map to -1 and are reported by the C-side
+            # validation, which checks groups before links like
+            # validate_spec (types.cpp:93-146). Duplicate names resolve to
+            # the first declaration (find_group, types.cpp:26-31).
             if L.scope == HP_INTER_GROUP:
                 a, b = _req(ep, "group_a", "cluster.link"), _req(ep, "group_b", "cluster.link")
-                if a not in idx or b not in idx:
-                    raise ConfigError("cluster: inter-group link references undeclared group")
-                L.group_a, L.group_b = idx[a], idx[b]
+                L.group_a, L.group_b = idx.get(a, -1), idx.get(b, -1)
             else:
                 a = _req(ep, "group", "cluster.link")
-                if a not in idx:
-                    raise ConfigError(f"cluster: link references unknown group '{a}'")
-                L.group_a, L.group_b = idx[a], -1
+                L.group_a, L.group_b = idx.get(a, -1), -1
             L.bandwidth_bits_per_s = float(_req(l, "bandwidth_bits_per_s", "cluster.link"))
             L.latency_s = float(l.get("latency_s", 0.0))
             pk = l.get("path_kind", "gpu-direct")

@@ -20,8 +20,11 @@ struct hp_ctx {
 
 namespace {
 
+thread_local std::string g_err;  // last error of calls made without a context
+
 hp_status fail(hp_ctx* ctx, const hph::Status& s) {
   if (ctx) ctx->err = s.msg;
+  else g_err = s.msg;
   return s.code;
 }
 
@@ -72,7 +75,7 @@ void hp_destroy(hp_ctx* ctx) {
   delete ctx;
 }
 
-const char* hp_last_error(const hp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+const char* hp_last_error(const hp_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
 
 hp_status hp_validate(hp_ctx* ctx, const hp_problem* problem) {
   hph::Problem p;

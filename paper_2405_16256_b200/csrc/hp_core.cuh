@@ -72,7 +72,7 @@ struct Leaf {
   int split_off;    // offset of this leaf's P-int rows in per-leaf split buffers
   int lg_off;       // offset of this leaf's LeafGroup rows (n_groups each)
   int mode;         // 0 hill climb, 1 exhaustive, 2 uniform only, 3 explicit plan
-  int pad;
+  int sched;        // hp_schedule of this leaf's candidates (explicit plans carry their own)
 };
 
 // ---------------------------------------------------------------- helpers

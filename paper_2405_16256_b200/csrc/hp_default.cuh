@@ -121,7 +121,7 @@ __device__ inline double incumbent(const TaskState& ts, double gb) {
 __device__ inline void simulate_list(const Bufs& b, int li, int kind, const long long* ids, int n,
                                      int out_base, int lane) {
   const Leaf lf = b.leaves[li];
-  const int cls = eval_class(lf.P, lf.M, c_consts.schedule == 0);
+  const int cls = eval_class(lf.P, lf.M, lf.sched == 0);
   const int cpw = class_cpw(cls, lf.P);
   for (int g = 0; g < n; g += cpw) {
     Work w;

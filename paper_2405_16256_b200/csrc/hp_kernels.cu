@@ -172,9 +172,9 @@ __device__ __forceinline__ int cand_count(const Bufs& b, const Leaf& lf, const W
 // Generic evaluator (GPipe, M < P): counter-driven readiness per level.
 template <int K>
 __device__ __forceinline__ void eval_item_generic(const Bufs& b, const Work& w, const int lane) {
-  const bool gpipe = c_consts.schedule == 0;
   {
     const Leaf lf = b.leaves[w.leaf];
+    const bool gpipe = lf.sched == 0;
     const int P = lf.P;
     const int M = lf.M;
     const int W2 = seg_width(P, K);
@@ -525,6 +525,7 @@ struct AsyncQ {
   unsigned long long* tail;  // next ticket to produce
   int* pending;              // per leaf: items of the current step not yet done
   int* active;               // leaves of this class still climbing
+  int* abort;                // watchdog flag
   unsigned long long cap;
 };
 
@@ -572,8 +573,16 @@ __global__ void __launch_bounds__(256) k_hill_async(Bufs b, AsyncQ q, int cls) {
       const unsigned long long k = h % q.cap;
       volatile unsigned long long* sq = q.seq + k;
       unsigned ns = 32;
+      const long long t0 = clock64();
       while (*sq != h + 1) {
-        if (*(volatile int*)q.active == 0) {
+        if (*(volatile int*)q.active == 0 || *(volatile int*)q.abort) {
+          quit = 1;
+          break;
+        }
+        // watchdog: a queue that stalls for ~30 s means a bookkeeping bug;
+        // abort instead of hanging the GPU (reported as HP_INTERNAL)
+        if (clock64() - t0 > (1LL << 36)) {
+          atomicExch(q.abort, 1);
           quit = 1;
           break;
         }
@@ -893,6 +902,7 @@ static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vect
     lf.split_off = split_total;
     lf.lg_off = k * G;
     lf.mode = p.uniform_only ? 2 : (h.exhaustive ? 1 : 0);
+    lf.sched = p.schedule;
     split_total += t.pp;
     for (int g = 0; g < G; ++g)
       lgs[(size_t)k * G + g] = hph::leaf_group(p, g, h.tp[g], h.B, h.dp, h.nodes[g]);
@@ -980,7 +990,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   std::vector<std::vector<Work>> seedq(hpk::NCLS);
   const bool gpipe = p.schedule == HP_GPIPE;
   for (int k : hill_ids) {
-    int cls = hpk::eval_class(leaves[k].P, leaves[k].M, gpipe);
+    int cls = hpk::eval_class(leaves[k].P, leaves[k].M, leaves[k].sched == 0);
     int cpw = hpk::class_cpw(cls, leaves[k].P);
     int n = p.uniform_only ? 1 : 2;
     if (cpw >= n) {
@@ -1023,7 +1033,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   std::vector<size_t> items_cls(hpk::NCLS, 0);
   for (int k : hill_ids) {
     if (leaves[k].mode != 0) continue;
-    int cls = hpk::eval_class(leaves[k].P, leaves[k].M, gpipe);
+    int cls = hpk::eval_class(leaves[k].P, leaves[k].M, leaves[k].sched == 0);
     by_cls[cls].push_back(k);
     int cpw = hpk::class_cpw(cls, leaves[k].P);
     items_cls[cls] += (2 * (leaves[k].P - 1) + cpw - 1) / cpw;
@@ -1040,6 +1050,8 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   q.head = d_q;
   q.tail = d_q + 1;
   q.active = reinterpret_cast<int*>(d_q + 2);
+  q.abort = reinterpret_cast<int*>(d_q + 3);
+  CK(cudaMemsetAsync(d_q, 0, sizeof(unsigned long long) * 4, st));
   q.pending = d_pending;
   q.cap = qcap;
   for (int cls = 0; cls < hpk::NCLS; ++cls) {
@@ -1048,7 +1060,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     std::string nm = "cls_ids" + std::to_string(cls);
     if (!(s = upload(a, nm.c_str(), by_cls[cls], &d_cls_ids)).ok()) return s;
     CK(cudaMemsetAsync(q.seq, 0, sizeof(unsigned long long) * qcap, st));
-    CK(cudaMemsetAsync(d_q, 0, sizeof(unsigned long long) * 4, st));
+    CK(cudaMemsetAsync(d_q, 0, sizeof(unsigned long long) * 3, st));
     int n = static_cast<int>(by_cls[cls].size());
     hpk::k_async_seed<<<(n + T - 1) / T, T, 0, st>>>(b, q, d_cls_ids, n, cls);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1062,6 +1074,12 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     out.eval_launches++;
   }
   out.hill_iterations = 0;
+  if (!by_cls.empty()) {
+    int abort_flag = 0;
+    CK(cudaMemcpyAsync(&abort_flag, q.abort, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (abort_flag) return hph::Status{HP_INTERNAL, "watchdog: hill-climb work queue stalled"};
+  }
 
   // ---- exhaustive leaves, in chunks of candidates
   if (!exh_ids.empty()) {
@@ -1080,7 +1098,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
         const Leaf& lf = leaves[k];
         long long total = p.leaves[my_leaves[k]].n_splits;
         long long take = std::min(total - pos, kChunk - used);
-        int cls = hpk::eval_class(lf.P, lf.M, gpipe);
+        int cls = hpk::eval_class(lf.P, lf.M, lf.sched == 0);
         int cpw = hpk::class_cpw(cls, lf.P);
         for (long long j = 0; j < take; j += cpw)
           q[cls].push_back(Work{k, 2, pos + j, (int)std::min<long long>(cpw, take - j), (int)(used + j), nullptr});
@@ -1175,6 +1193,7 @@ hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans
     lf.split_off = static_cast<int>(splits.size());
     lf.lg_off = static_cast<int>(lgs.size());
     lf.mode = 3;
+    lf.sched = pl.schedule;
     for (size_t l = 0; l < p.links.size(); ++l) hop[(size_t)k * p.links.size() + l] = hph::hop_time(p, (int)l, B);
     for (int i = 0; i < P; ++i) {
       const hp_stage& s = pl.stages[i];
@@ -1182,7 +1201,7 @@ hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans
       splits.push_back(s.layer_end - s.layer_begin);
       lgs.push_back(hph::leaf_group(p, s.group, s.tp_degree, B, s.dp_degree, s.nodes_used));
     }
-    q[hpk::eval_class(P, lf.M, p.schedule == HP_GPIPE)].push_back(Work{k, 0, 0, 1, 0, nullptr});
+    q[hpk::eval_class(P, lf.M, lf.sched == HP_GPIPE)].push_back(Work{k, 0, 0, 1, 0, nullptr});
   }
   hpk::Bufs b{};
   hph::Status s;

@@ -194,7 +194,8 @@ HPD void hill_init(const Consts& c, const Leaf& lf, const LeafGroup* lg, const u
     hs.cur_time = t_uni;
     for (int i = 0; i < P; ++i) cur[i] = uni[i];
   }
-  hs.active = hs.start != 0 && 4 * c.L > 0;
+  // a single stage has no neighbours: the loop body finds none and stops
+  hs.active = hs.start != 0 && P > 1 && 4 * c.L > 0;
 }
 
 // Marks old[q] for neighbours of cur that the reference's memo already holds

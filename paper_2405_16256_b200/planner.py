@@ -151,25 +151,16 @@ def reduce_results(problem: abi.Problem, results: List[abi.hp_result]) -> abi.hp
     return out
 
 
-def search_sharded(docs: Dict[str, dict], rank: int, world: int, device: int, group=None) -> SearchOutcome:
-    """One shard per rank; the per-rank hp_result records (fixed size) are
-    all-gathered over NCCL/NVLink in one collective and every rank applies
-    the same exact reduction, so all ranks return the same plan."""
+def gather_results(res: abi.hp_result, world: int, group=None, device=None) -> List[abi.hp_result]:
+    """All-gathers the fixed-size per-rank hp_result records in one
+    collective (NCCL over NVLink with CUDA tensors; gloo with CPU tensors)."""
     import torch
     import torch.distributed as dist
 
-    problem = abi.Problem(docs)
-    eng = engine(device)
-    bound = None
-    if problem.struct.planner.time_bound_pruning:
-        b = eng.probe_shard(problem, rank, world)
-        t = torch.tensor([b], dtype=torch.float64, device=f"cuda:{device}")
-        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
-        bound = float(t.item())
-    res = eng.search_shard(problem, rank, world, bound)
     nbytes = C.sizeof(abi.hp_result)
-    mine = torch.frombuffer(bytearray(C.string_at(C.byref(res), nbytes)), dtype=torch.uint8).to(f"cuda:{device}")
-    gathered = torch.empty(world * nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+    dev = f"cuda:{device}" if device is not None else "cpu"
+    mine = torch.frombuffer(bytearray(C.string_at(C.byref(res), nbytes)), dtype=torch.uint8).to(dev)
+    gathered = torch.empty(world * nbytes, dtype=torch.uint8, device=dev)
     dist.all_gather_into_tensor(gathered, mine, group=group)
     host = gathered.cpu().numpy().tobytes()
     recs = []
@@ -177,7 +168,33 @@ def search_sharded(docs: Dict[str, dict], rank: int, world: int, device: int, gr
         rec = abi.hp_result()
         C.memmove(C.byref(rec), host[r * nbytes:(r + 1) * nbytes], nbytes)
         recs.append(rec)
-    red = reduce_results(problem, recs)
+    return recs
+
+
+def search_sharded(docs: Dict[str, dict], rank: int, world: int, device: Optional[int] = None, group=None,
+                   shard_fn=None, probe_fn=None) -> SearchOutcome:
+    """One shard per rank; default mode first all-reduces (MIN) the per-shard
+    probe bounds (planner.cpp:640-651), then every rank searches its shard and
+    the per-rank records are all-gathered in one collective; every rank
+    applies the same exact reduction, so all ranks return the same plan.
+    shard_fn/probe_fn replace the GPU engine (tests drive the CPU emulation
+    through the same reduction with gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    problem = abi.Problem(docs)
+    if shard_fn is None:
+        eng = engine(device)
+        shard_fn = lambda p, r, w, b: eng.search_shard(p, r, w, b)  # noqa: E731
+        probe_fn = lambda p, r, w: eng.probe_shard(p, r, w)  # noqa: E731
+    bound = None
+    if problem.struct.planner.time_bound_pruning:
+        b = probe_fn(problem, rank, world)
+        t = torch.tensor([b], dtype=torch.float64, device=f"cuda:{device}" if device is not None else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        bound = float(t.item())
+    res = shard_fn(problem, rank, world, bound)
+    red = reduce_results(problem, gather_results(res, world, group, device))
     if not red.has_best:
         raise abi.InfeasibleError("no feasible plan found")
     return _outcome(problem, red)

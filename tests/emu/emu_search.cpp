@@ -37,7 +37,7 @@ double eval(const Consts& c, const LeafDev& L, const int* split) {
 
 }  // namespace
 
-extern "C" int emu_search(const hp_problem* in, hp_result* res) {
+extern "C" int emu_search_shard(const hp_problem* in, int shard, int count, hp_result* res) {
   hph::Problem p;
   hph::Status s = hph::load_problem(in, p);
   if (!s.ok()) return s.code;
@@ -51,6 +51,7 @@ extern "C" int emu_search(const hp_problem* in, hp_result* res) {
     for (size_t l = 0; l < p.links.size(); ++l) hop[b * p.links.size() + l] = hph::hop_time(p, (int)l, p.mbs[b]);
   std::memset(res, 0, sizeof(*res));
   res->tasks = (long long)p.tasks.size();
+  if (shard == 0)
   for (const hph::Task& t : p.tasks)
     if (t.no_link) { res->candidates_pruned++; res->reason_counts[HP_REASON_NO_LINK]++; }
     else if (t.leaf_begin == t.leaf_end) { res->candidates_pruned++; res->reason_counts[HP_REASON_NO_ASSIGNMENT]++; }
@@ -60,7 +61,7 @@ extern "C" int emu_search(const hp_problem* in, hp_result* res) {
   LeafDev best_leaf;
   std::vector<int> best_split;
   int best_li = -1;
-  for (int li = 0; li < (int)p.leaves.size(); ++li) {
+  for (int li : hph::shard_leaves(p, shard, count)) {
     const hph::LeafHost& h = p.leaves[li];
     const hph::Task& t = p.tasks[h.task];
     LeafDev L;
@@ -116,10 +117,41 @@ extern "C" int emu_search(const hp_problem* in, hp_result* res) {
       have = true; best_t = hs.best_time; best_leaf = L; best_split = bs; best_li = li;
     }
   }
-  if (!have) return HP_INFEASIBLE;
+  if (!have) return count > 1 ? HP_OK : HP_INFEASIBLE;
   res->has_best = 1;
   res->best_time_s = best_t;
   res->best_pp = best_leaf.lf.P;
   hph::make_plan(p, p.leaves[best_li], best_split.data(), res->best_plan);
   return HP_OK;
+}
+
+extern "C" int emu_search(const hp_problem* in, hp_result* res) { return emu_search_shard(in, 0, 1, res); }
+
+// Explicit-plan evaluation through the same per-stage setup + serial
+// level-synchronous simulation (mode 3 pseudo-leaf, like hp_evaluate_plans).
+extern "C" int emu_evaluate(const hp_problem* in, const hp_plan* plan, double* out) {
+  hph::Problem p;
+  hph::Status s = hph::load_problem(in, p);
+  if (!s.ok()) return s.code;
+  Consts c;
+  hph::fill_consts(p, c);
+  const int P = plan->n_stages;
+  int64_t B = plan->micro_batch_size > 0 ? plan->micro_batch_size : p.train.micro_batch_size;
+  Leaf lf{-1, P, (int)plan->micro_batches_per_dp_replica, plan->stages[0].dp_degree, B, 0, 0, 0, 0, 3, 0};
+  std::vector<LeafGroup> lg;
+  std::vector<uint8_t> slots;
+  std::vector<double> hop(p.links.size());
+  for (size_t l = 0; l < p.links.size(); ++l) hop[l] = hph::hop_time(p, (int)l, B);
+  for (int i = 0; i < P; ++i) {
+    const hp_stage& st = plan->stages[i];
+    lg.push_back(hph::leaf_group(p, st.group, st.tp_degree, B, st.dp_degree, st.nodes_used));
+    slots.push_back((uint8_t)i);
+  }
+  std::vector<StageDur> d(P);
+  std::vector<StageState> ss(P);
+  for (int i = 0; i < P; ++i)
+    stage_setup(c, lf, lg.data(), slots.data(), hop.data(), i,
+                plan->stages[i].layer_end - plan->stages[i].layer_begin, d[i]);
+  *out = simulate_serial(c.schedule == 0 || plan->schedule == HP_GPIPE, P, lf.M, d.data(), ss.data());
+  return 0;
 }

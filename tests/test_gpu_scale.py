@@ -1,0 +1,66 @@
+"""Full-size properties on the B200 (sizes the CPU oracle cannot finish in a
+test): the C3 Llama-140B / 768-device full strategy sweep, determinism,
+shard-count invariance of the reduction, and agreement with the
+time-bound-pruned search (whose C3 outcome is pinned by the reference)."""
+from __future__ import annotations
+
+import json
+import os
+
+import pytest
+
+from conftest import GOLDEN
+from paper_2405_16256_b200 import abi, configs, planner
+
+pytestmark = pytest.mark.gpu
+
+C3_PLAN = ("1f1b|192|1|gpu_a:0-12:8:8:8|gpu_a:12-24:8:8:8|gpu_a:24-36:8:8:8|gpu_a:36-47:8:8:8|gpu_a:47-59:8:8:8|"
+           "gpu_a:59-70:8:8:8|gpu_a:70-82:8:8:8|gpu_a:82-94:8:8:8|gpu_a:94-105:8:8:8|gpu_a:105-115:8:8:8|"
+           "amd:115-138:8:8:8|amd:138-160:8:8:8")
+C3_TIME = 138.65139569127317  # reference, C3 default mode
+
+
+def test_c3_default_mode_matches_reference_numbers(engine):
+    """the reference's C3 default search simulates 1,866 and
+    prunes 216,837 candidates and picks pp12 dp8 tp8 M192 at 138.651396 s."""
+    p = abi.Problem(configs.config("C3", full=False))
+    r = engine.search_shard(p)
+    assert (r.candidates_simulated, r.candidates_pruned) == (1866, 216837)
+    assert r.best_time_s == C3_TIME
+    assert abi.encode_plan(p.group_names, r.best_plan) == C3_PLAN
+
+
+def test_c3_full_sweep(engine):
+    p = abi.Problem(configs.config("C3", full=True))
+    a = engine.search_shard(p)
+    b = engine.search_shard(p)
+    # deterministic, and the full sweep finds the same optimum as the pruned
+    # search (the bound is admissible and this instance has no hill-climb
+    # divergence at the optimum)
+    assert a.best_time_s == b.best_time_s == C3_TIME
+    assert abi.encode_plan(p.group_names, a.best_plan) == C3_PLAN
+    assert (a.candidates_simulated, a.candidates_pruned) == (b.candidates_simulated, b.candidates_pruned)
+    pinned = os.path.join(GOLDEN, "c3_full_counts.json")
+    if os.path.exists(pinned):
+        want = json.load(open(pinned))
+        assert (a.candidates_simulated, a.candidates_pruned) == (want["candidates_simulated"],
+                                                                 want["candidates_pruned"])
+
+
+@pytest.mark.parametrize("count", [2, 3, 8])
+def test_shard_reduction_invariance(engine, count):
+    """N shards on one GPU, reduced exactly, equal the unsharded search
+    (what the 8-GPU NCCL path computes)."""
+    for full in (True, False):
+        docs = configs.with_pp(configs.config("C3", full=full), [10, 12, 20])
+        p = abi.Problem(docs)
+        whole = engine.search_shard(p)
+        bound = None
+        if not full:
+            bound = min(engine.probe_shard(p, s, count) for s in range(count))
+        parts = [engine.search_shard(p, s, count, bound) for s in range(count)]
+        red = planner.reduce_results(p, parts)
+        assert red.best_time_s == whole.best_time_s
+        assert (red.candidates_simulated, red.candidates_pruned) == (whole.candidates_simulated,
+                                                                     whole.candidates_pruned)
+        assert abi.encode_plan(p.group_names, red.best_plan) == abi.encode_plan(p.group_names, whole.best_plan)
