@@ -37,9 +37,11 @@ METRIC = "candidate plans evaluated/sec (Llama-140B, 768 dev); time-to-optimal-p
 UNIT = "candidates/s"
 WORKLOAD = ("C3: Llama-140B (L=160, H=8192, seq 4096) on 768 devices (amd 16x8 + gpu_a 80x8), "
             "G=1536, B in {1,2}, pp 1..96, full strategy sweep (time_bound_pruning=false)")
-# Deterministic CPU sample of the same sweep (pipeline degrees spread over the
-# range that has feasible candidates); see DESIGN.md "CPU baseline".
-CPU_SAMPLE_PP = [12, 24]
+# Deterministic, work-matched CPU sample of the same sweep: pipeline degrees
+# {12, 29, 96} hold 109,719 of the 10,513,178 candidates and their mean
+# simulated P*M per candidate is 66,321 vs 66,314 for the whole sweep (per-pp
+# counts of tests/golden/c3_full_counts.json); see DESIGN.md "CPU baseline".
+CPU_SAMPLE_PP = [12, 29, 96]
 
 
 def parse():
@@ -307,6 +309,11 @@ def main_ours(args):
         try:
             cb = cpu_baseline(os.cpu_count() or 1)
             cb["cpu"] = cpu_model()
+            # this GPU on exactly the CPU sample, for an apples-to-apples ratio
+            ps = abi.Problem(cpu_sample_cfg())
+            rs = eng.search_shard(ps)
+            cb["gpu_same_sample"] = {"value": (rs.candidates_simulated + rs.candidates_pruned) /
+                                              (rs.device_ms / 1e3), "unit": UNIT, "device_ms": rs.device_ms}
             line["cpu_baseline"] = cb
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "error": str(e)}
