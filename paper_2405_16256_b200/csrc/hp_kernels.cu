@@ -405,66 +405,71 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
     }
     const int T = 2 * (M + P - 1);
     const int core_lo = 2 * P, core_hi = 2 * M - 2;  // every stage busy
-    // one edge (predicated) level
-    auto edge = [&](int t) {
-      const double lchf = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
-      const double rchb = __shfl_sync(0xffffffffu, chb[0], src_r);
-      double pchf[K], pchb[K];
-#pragma unroll
-      for (int r = 0; r < K; ++r) {
-        pchf[r] = chf[r];
-        pchb[r] = chb[r];
-      }
-#pragma unroll
-      for (int r = 0; r < K; ++r) {
-        const int i = sl * K + r;
-        const bool isF = ((t - r) & 1) == 0;  // (t - i) even, i - r even
-        const bool act = isF ? (t >= 2 * P - i && t <= 2 * M - 2 + i)
-                             : (t >= 2 * P - 1 - i && t <= 2 * M + 2 * P - 3 - i);
-        const double recv = isF ? (r == 0 ? lchf : pchf[r > 0 ? r - 1 : 0])
-                                : (r == K - 1 ? rchb : pchb[r < K - 1 ? r + 1 : 0]);
-        const double nfr = dmax(fr[r], recv) + (isF ? f[r] : bw[r]);
-        const double nch = dmax(nfr, isF ? chf[r] : chb[r]) + (isF ? sf[r] : sb[r]);
-        if (act) {
-          fr[r] = nfr;
-          if (isF) chf[r] = nch;
-          else chb[r] = nch;
-        }
-      }
-    };
-    // one core level of parity PAR: stage r runs F iff (PAR - r) is even;
-    // neighbours run the opposite op, so no snapshot is needed.
-    auto core = [&](auto par_tag) {
+    // One level of parity PAR after the warm-up: stage r runs F iff
+    // (PAR - r) is even (i = sl*K + r with K even), B otherwise; adjacent
+    // stages always run opposite ops, so nothing needs a snapshot. PRED
+    // levels (transition and cool-down windows) gate each op on its closed
+    // form window with selects; core levels run every op unconditionally.
+    auto level = [&](auto par_tag, auto pred_tag, int t) {
       constexpr int PAR = decltype(par_tag)::value;
+      constexpr bool PRED = decltype(pred_tag)::value;
       const double lchf = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
       const double rchb = __shfl_sync(0xffffffffu, chb[0], src_r);
+      const int u0 = t + sl * K;  // t + i - r
+      const int v0 = t - sl * K;  // t - i + r
 #pragma unroll
       for (int r = 0; r < K; ++r) {
         if (((PAR - r) & 1) == 0) {
           const double recv = r == 0 ? lchf : chf[r > 0 ? r - 1 : 0];
-          fr[r] = dmax(fr[r], recv) + f[r];
-          chf[r] = dmax(fr[r], chf[r]) + sf[r];
+          const double nfr = dmax(fr[r], recv) + f[r];
+          const double nch = dmax(nfr, chf[r]) + sf[r];
+          if (PRED) {
+            // F(i,m) at level 2m+i: 2P-i <= t <= 2M-2+i
+            const bool act = (u0 + r >= 2 * P) && (v0 - r <= 2 * M - 2);
+            fr[r] = act ? nfr : fr[r];
+            chf[r] = act ? nch : chf[r];
+          } else {
+            fr[r] = nfr;
+            chf[r] = nch;
+          }
         } else {
           const double recv = r == K - 1 ? rchb : chb[r < K - 1 ? r + 1 : 0];
-          fr[r] = dmax(fr[r], recv) + bw[r];
-          chb[r] = dmax(fr[r], chb[r]) + sb[r];
+          const double nfr = dmax(fr[r], recv) + bw[r];
+          const double nch = dmax(nfr, chb[r]) + sb[r];
+          if (PRED) {
+            // B(i,j) at level 2P-1-i+2j: 2P-1-i <= t <= 2M+2P-3-i
+            const bool act = (u0 + r >= 2 * P - 1) && (u0 + r <= 2 * M + 2 * P - 3);
+            fr[r] = act ? nfr : fr[r];
+            chb[r] = act ? nch : chb[r];
+          } else {
+            fr[r] = nfr;
+            chb[r] = nch;
+          }
         }
       }
     };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using PT = std::true_type;
+    using PF = std::false_type;
+    auto pred_level = [&](int t) {
+      if (t & 1) level(I1{}, PT{}, t);
+      else level(I0{}, PT{}, t);
+    };
     int t = P;
-    for (; t < T && t < core_lo; ++t) edge(t);
+    for (; t < T && t < core_lo; ++t) pred_level(t);
     if (core_lo <= core_hi) {
       // core_lo is even: pairs (even, odd), then the final even level
       for (; t + 1 <= core_hi; t += 2) {
-        core(std::integral_constant<int, 0>{});
-        core(std::integral_constant<int, 1>{});
+        level(I0{}, PF{}, t);
+        level(I1{}, PF{}, t + 1);
       }
       if (t <= core_hi) {
-        core(std::integral_constant<int, 0>{});
+        level(I0{}, PF{}, t);
         ++t;
       }
     }
-    for (; t < T; ++t) edge(t);
+    for (; t < T; ++t) pred_level(t);
   }
   double v = 0.0;
 #pragma unroll
