@@ -79,7 +79,22 @@ struct Bufs {
   double* xbuf;
   HillState* hs;
   unsigned long long* ops;  // algorithmic FP64 add/max ops of simulated candidates
+  // exhaustive regime: per-leaf bounded-composition tables (exh_table) and
+  // memory caps; ranks of kind-2 work items index the bounded compositions
+  const long long* etbl;
+  const int* etbl_off;
+  const int* ecap;
 };
+
+// count of bounded compositions continuing with part value v at position j
+__device__ __forceinline__ long long exh_count(const Bufs& b, const Leaf& lf, int leaf, int j, int rem,
+                                               int v) {
+  if (b.etbl == nullptr) return binom(rem - v - 1, lf.P - j - 2);  // unbounded (default mode)
+  const int W = c_consts.L + 1;
+  const int cap = b.ecap[lf.split_off + j];
+  if (v > cap || rem - v < 0) return 0;
+  return b.etbl[b.etbl_off[leaf] + (j + 1) * W + rem - v];
+}
 
 __device__ __forceinline__ int next_pow2(int v) {
   int p = 1;
@@ -201,7 +216,7 @@ __device__ __forceinline__ void eval_item_generic(const Bufs& b, const Work& w, 
         } else {
           int left = P - j;
           for (v = 1;; ++v) {
-            long long cntv = binom(rem - v - 1, left - 2);
+            long long cntv = exh_count(b, lf, w.leaf, j, rem, v);
             if (rank < cntv) break;
             rank -= cntv;
           }
@@ -330,7 +345,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
       } else {
         int left = P - j;
         for (v = 1;; ++v) {
-          long long cntv = binom(rem - v - 1, left - 2);
+          long long cntv = exh_count(b, lf, w.leaf, j, rem, v);
           if (rank < cntv) break;
           rank -= cntv;
         }
@@ -685,17 +700,302 @@ __global__ void k_exh_reduce(Bufs b, const ExhSpan* spans, int n_spans) {
     }
     hs.simulated++;
     bool better = !hs.has_best || t < hs.best_time;
+    const int* caps = b.ecap + lf.split_off;
+    const long long* tbl = b.etbl + b.etbl_off[sp.leaf];
     if (!better && t == hs.best_time) {
-      unrank_composition(sp.first + j, c_consts.L, lf.P, comp);
+      unrank_bounded(sp.first + j, c_consts.L, lf.P, caps, tbl, comp);
       better = split_enc_less(lf.P, comp, best);
     }
     if (better) {
       hs.has_best = 1;
       hs.best_time = t;
-      unrank_composition(sp.first + j, c_consts.L, lf.P, best);
+      unrank_bounded(sp.first + j, c_consts.L, lf.P, caps, tbl, best);
     }
   }
   b.hs[sp.leaf] = hs;
+}
+
+// ------------------------------------------------------------------ exhaustive (bounded)
+
+// Per exhaustive leaf: memory caps, bounded-composition table, feasible count.
+__global__ void k_exh_prep(Bufs b, const int* ids, int n, long long* feas, long long* etbl, int* ecap) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int li = ids[k];
+  const Leaf lf = b.leaves[li];
+  int* caps = ecap + lf.split_off;
+  exh_caps(c_consts, lf, b.lg + lf.lg_off, b.layouts + lf.layout_off, caps);
+  feas[li] = exh_table(c_consts.L, lf.P, caps, etbl + b.etbl_off[li]);
+}
+
+struct ExhItem {
+  int leaf;
+  int pad;
+  long long first;  // first bounded rank
+  long long n;      // ranks in this item (<= 32 * kExhChunk)
+};
+
+struct ExhRec {
+  double t;
+  long long rank;
+  long long sim;
+  int leaf;
+  int has;
+};
+
+constexpr int kExhChunk = 64;  // consecutive ranks per thread
+
+// decimal-string order of two ints followed by ':' (encode_plan fields)
+__device__ __forceinline__ bool dec_less(long long x, long long y) {
+  char da[24], db[24];
+  const int na = fmt_ll(x, da), nb = fmt_ll(y, db);
+  for (int k = 0;; ++k) {
+    const int u = k < na ? (unsigned char)da[k] : ':';
+    const int v = k < nb ? (unsigned char)db[k] : ':';
+    if (u != v) return u < v;
+    if (k >= na && k >= nb) return false;
+  }
+}
+
+template <int P>
+__device__ __forceinline__ bool enc_less_t(const int (&a)[P], const int (&b)[P]) {
+  int s = 0;
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    if (a[i] != b[i]) return dec_less(s + a[i], s + b[i]);
+    s += a[i];
+  }
+  return false;
+}
+
+template <int P>
+__device__ __forceinline__ void unrank_bounded_t(long long rank, int L, const int (&caps)[P],
+                                                 const long long* tbl, int (&out)[P]) {
+  const int W = L + 1;
+  int rem = L;
+#pragma unroll
+  for (int j = 0; j < P - 1; ++j) {
+    for (int v = 1;; ++v) {
+      long long cnt = (v <= caps[j] && rem - v >= 0) ? tbl[(j + 1) * W + rem - v] : 0;
+      if (rank < cnt) {
+        out[j] = v;
+        rem -= v;
+        break;
+      }
+      rank -= cnt;
+    }
+  }
+  out[P - 1] = rem;
+}
+
+template <int P>
+__device__ __forceinline__ bool next_bounded_t(int (&c)[P], const int (&caps)[P], const int (&sufcap)[P + 1]) {
+  int suffix = c[P - 1];
+#pragma unroll
+  for (int j = P - 2; j >= 0; --j) {
+    const int rest = suffix - 1;
+    if (c[j] + 1 <= caps[j] && rest >= P - 1 - j && rest <= sufcap[j + 1]) {
+      c[j] += 1;
+      int r = rest;
+#pragma unroll
+      for (int k = j + 1; k < P - 1; ++k) {
+        int v = r - sufcap[k + 1];
+        if (v < 1) v = 1;
+        c[k] = v;
+        r -= v;
+      }
+      c[P - 1] = r;
+      return true;
+    }
+    suffix += c[j];
+  }
+  return false;
+}
+
+// Serial closed-form 1F1B (M >= P) for a compile-time P, state in registers.
+// All threads of a warp share (P, M), so every phase test is warp-uniform.
+template <int P>
+__device__ __forceinline__ double sim_thread(int M, const double (&f)[P], const double (&bw)[P],
+                                             const double (&sf)[P], const double (&sb)[P],
+                                             const double (&dps)[P]) {
+  double fr[P], chf[P], chb[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) fr[i] = chf[i] = chb[i] = 0.0;
+  for (int t = 0; t < P; ++t) {  // warm-up: F(i, t-i) for i <= t
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) {
+      if (i <= t) {
+        fr[i] = (i == 0 ? fr[i] : dmax(fr[i], chf[i > 0 ? i - 1 : 0])) + f[i];
+        if (i < P - 1) chf[i] = dmax(fr[i], chf[i]) + sf[i];
+      }
+    }
+  }
+  const int T = 2 * (M + P - 1);
+  auto lvl = [&](auto par_tag, auto pred_tag, int t) {
+    constexpr int PAR = decltype(par_tag)::value;
+    constexpr bool PRED = decltype(pred_tag)::value;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      if (((PAR - i) & 1) == 0) {
+        if (!PRED || (t >= 2 * P - i && t <= 2 * M - 2 + i)) {
+          fr[i] = (i == 0 ? fr[i] : dmax(fr[i], chf[i > 0 ? i - 1 : 0])) + f[i];
+          if (i < P - 1) chf[i] = dmax(fr[i], chf[i]) + sf[i];
+        }
+      } else {
+        if (!PRED || (t >= 2 * P - 1 - i && t <= 2 * M + 2 * P - 3 - i)) {
+          fr[i] = (i == P - 1 ? fr[i] : dmax(fr[i], chb[i < P - 1 ? i + 1 : 0])) + bw[i];
+          if (i > 0) chb[i] = dmax(fr[i], chb[i]) + sb[i];
+        }
+      }
+    }
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  int t = P;
+  for (; t < T && t < 2 * P; ++t) {
+    if (t & 1) lvl(I1{}, std::true_type{}, t);
+    else lvl(I0{}, std::true_type{}, t);
+  }
+  const int core_hi = 2 * M - 2;
+  for (; t + 1 <= core_hi; t += 2) {
+    lvl(I0{}, std::false_type{}, t);
+    lvl(I1{}, std::false_type{}, t + 1);
+  }
+  for (; t < T; ++t) {
+    if (t & 1) lvl(I1{}, std::true_type{}, t);
+    else lvl(I0{}, std::true_type{}, t);
+  }
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    v = dmax(v, fr[i]);
+    v = dmax(v, fr[i] + dps[i]);
+    if (i < P - 1) v = dmax(v, chf[i]);
+    if (i > 0) v = dmax(v, chb[i]);
+  }
+  return v;
+}
+
+// Thread-per-candidate exhaustive evaluation (1F1B, M >= P, P <= 8): a warp
+// owns one item of consecutive bounded ranks, each thread kExhChunk of them
+// walked with next_bounded; per-thread exact argmin, then warp argmin.
+template <int P>
+__global__ void __launch_bounds__(128) k_exh_thread(Bufs b, const ExhItem* items, int n_items,
+                                                    ExhRec* recs) {
+  const int lane = threadIdx.x & 31;
+  const int it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (it >= n_items) return;
+  const ExhItem w = items[it];
+  const Leaf lf = b.leaves[w.leaf];
+  const LeafGroup* lg = b.lg + lf.lg_off;
+  const uint8_t* slots = b.layouts + lf.layout_off;
+  const double* hop = b.hop + lf.B_idx * c_consts.n_links;
+  const int L = c_consts.L;
+  const long long* tbl = b.etbl + b.etbl_off[w.leaf];
+  int caps[P], sufcap[P + 1];
+  sufcap[P] = 0;
+#pragma unroll
+  for (int i = P - 1; i >= 0; --i) {
+    caps[i] = b.ecap[lf.split_off + i];
+    sufcap[i] = sufcap[i + 1] + caps[i];
+  }
+  double fl[P], bl[P], sf[P], sb[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    const LeafGroup& row = lg[slots[i]];
+    fl[i] = row.fl;
+    bl[i] = row.bl;
+    sf[i] = i + 1 < P ? hop[c_consts.link_pair[row.group][lg[slots[i + 1]].group]] : 0.0;
+    sb[i] = i > 0 ? hop[c_consts.link_pair[lg[slots[i - 1]].group][row.group]] : 0.0;
+  }
+  const long long r0 = w.first + (long long)lane * kExhChunk;
+  long long cnt = w.first + w.n - r0;
+  if (cnt > kExhChunk) cnt = kExhChunk;
+  double bt = 0.0;
+  long long brank = -1;
+  int bcomp[P], comp[P];
+  long long sim = 0;
+  if (cnt > 0) unrank_bounded_t<P>(r0, L, caps, tbl, comp);
+  for (long long k = 0; k < cnt; ++k) {
+    if (k) next_bounded_t<P>(comp, caps, sufcap);
+    double f[P], bw[P], dps[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const LeafGroup& row = lg[slots[i]];
+      double layers = comp[i];
+      if (i == 0) layers += c_consts.edge;
+      if (i == P - 1) layers += c_consts.edge;
+      f[i] = layers * fl[i];
+      bw[i] = layers * bl[i];
+      dps[i] = dp_sync(row, comp[i]);
+    }
+    const double t = sim_thread<P>(lf.M, f, bw, sf, sb, dps);
+    ++sim;
+    if (brank < 0 || t < bt || (t == bt && enc_less_t<P>(comp, bcomp))) {
+      bt = t;
+      brank = r0 + k;
+#pragma unroll
+      for (int i = 0; i < P; ++i) bcomp[i] = comp[i];
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+    const long long orank = __shfl_xor_sync(0xffffffffu, brank, off);
+    int ocomp[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) ocomp[i] = __shfl_xor_sync(0xffffffffu, bcomp[i], off);
+    sim += __shfl_xor_sync(0xffffffffu, sim, off);
+    const bool take = orank >= 0 && (brank < 0 || ot < bt || (ot == bt && enc_less_t<P>(ocomp, bcomp)));
+    if (take) {
+      bt = ot;
+      brank = orank;
+#pragma unroll
+      for (int i = 0; i < P; ++i) bcomp[i] = ocomp[i];
+    }
+  }
+  if (lane == 0) {
+    recs[it] = ExhRec{bt, brank, sim, w.leaf, brank >= 0 ? 1 : 0};
+    if (b.ops) atomicAdd(b.ops, (unsigned long long)sim * (unsigned long long)(8LL * P * lf.M - 4LL * lf.M));
+  }
+}
+
+// Per leaf: merge its item records (exact comparator, ties re-unranked).
+__global__ void k_exh_merge(Bufs b, const ExhRec* recs, const int* rec_begin, const int* rec_end,
+                            const int* ids, int n) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int li = ids[k];
+  const Leaf lf = b.leaves[li];
+  const int* caps = b.ecap + lf.split_off;
+  const long long* tbl = b.etbl + b.etbl_off[li];
+  HillState hs = b.hs[li];
+  int* best = b.best + lf.split_off;
+  int tmp[HP_MAX_STAGES];
+  for (int r = rec_begin[k]; r < rec_end[k]; ++r) {
+    const ExhRec e = recs[r];
+    hs.simulated += e.sim;
+    if (!e.has) continue;
+    bool better = !hs.has_best || e.t < hs.best_time;
+    if (!better && e.t == hs.best_time) {
+      unrank_bounded(e.rank, c_consts.L, lf.P, caps, tbl, tmp);
+      better = split_enc_less(lf.P, tmp, best);
+    }
+    if (better) {
+      hs.has_best = 1;
+      hs.best_time = e.t;
+      unrank_bounded(e.rank, c_consts.L, lf.P, caps, tbl, best);
+    }
+  }
+  b.hs[li] = hs;
+}
+
+// Memory-pruned compositions of every exhaustive leaf, counted analytically.
+__global__ void k_exh_fix(Bufs b, const int* ids, int n, const long long* feas) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int li = ids[k];
+  const Leaf lf = b.leaves[li];
+  b.hs[li].pruned += contiguous_split_count(c_consts.L, lf.P) - feas[li];
 }
 
 // ------------------------------------------------------------------ final
@@ -831,6 +1131,12 @@ static hph::Status scratch(Arena& a, const char* name, size_t n, T** out) {
   hph::Status s = a.get(name, std::max<size_t>(1, n) * sizeof(T), &p);
   *out = static_cast<T*>(p);
   return s;
+}
+
+static size_t split_total_of(const std::vector<Leaf>& leaves) {
+  size_t n = 0;
+  for (const Leaf& lf : leaves) n += lf.P;
+  return n;
 }
 
 static void launch_eval(int cls, const hpk::Bufs& b, const Work* items, const int* n_items,
@@ -1086,42 +1392,146 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     if (abort_flag) return hph::Status{HP_INTERNAL, "watchdog: hill-climb work queue stalled"};
   }
 
-  // ---- exhaustive leaves, in chunks of candidates
+  // ---- exhaustive leaves: bounded compositions only (memory gate solved
+  // analytically), thread-per-candidate for small P, warp segments otherwise
   if (!exh_ids.empty()) {
-    const long long kChunk = 1 << 24;
-    double* d_x;
-    if (!(s = scratch(a, "xbuf", kChunk, &d_x)).ok()) return s;
-    b.xbuf = d_x;
-    size_t e = 0;
-    long long pos = 0;  // rank position within exh_ids[e]
-    while (e < exh_ids.size()) {
-      std::vector<std::vector<Work>> q(hpk::NCLS);
-      std::vector<hpk::ExhSpan> spans;
-      long long used = 0;
-      while (e < exh_ids.size() && used < kChunk) {
-        int k = exh_ids[e];
-        const Leaf& lf = leaves[k];
-        long long total = p.leaves[my_leaves[k]].n_splits;
-        long long take = std::min(total - pos, kChunk - used);
-        int cls = hpk::eval_class(lf.P, lf.M, lf.sched == 0);
-        int cpw = hpk::class_cpw(cls, lf.P);
-        for (long long j = 0; j < take; j += cpw)
-          q[cls].push_back(Work{k, 2, pos + j, (int)std::min<long long>(cpw, take - j), (int)(used + j), nullptr});
-        spans.push_back(hpk::ExhSpan{k, (int)used, pos, take});
-        used += take;
-        pos += take;
-        if (pos == total) {
-          ++e;
-          pos = 0;
-        }
-      }
-      if (!(s = run_queues(q, "exhq")).ok()) return s;
-      hpk::ExhSpan* d_spans;
-      if (!(s = upload(a, "spans", spans, &d_spans)).ok()) return s;
-      hpk::k_exh_reduce<<<((int)spans.size() + T - 1) / T, T, 0, st>>>(b, d_spans, (int)spans.size());
-      out.launches++;
-      CK(cudaStreamSynchronize(st));
+    const int L = p.model.num_layers;
+    std::vector<int> etbl_off(nL, 0);
+    size_t etbl_total = 0;
+    for (int k : exh_ids) {
+      etbl_off[k] = static_cast<int>(etbl_total);
+      etbl_total += (size_t)(leaves[k].P + 1) * (L + 1);
     }
+    int* d_etbl_off;
+    long long* d_etbl;
+    int* d_ecap;
+    long long* d_feas;
+    int* d_exh_ids;
+    if (!(s = upload(a, "etbl_off", etbl_off, &d_etbl_off)).ok()) return s;
+    if (!(s = scratch(a, "etbl", etbl_total, &d_etbl)).ok()) return s;
+    if (!(s = scratch(a, "ecap", split_total_of(leaves), &d_ecap)).ok()) return s;
+    if (!(s = scratch(a, "feas", nL, &d_feas)).ok()) return s;
+    if (!(s = upload(a, "exh_ids", exh_ids, &d_exh_ids)).ok()) return s;
+    b.etbl = d_etbl;
+    b.etbl_off = d_etbl_off;
+    b.ecap = d_ecap;
+    const int ne = static_cast<int>(exh_ids.size());
+    hpk::k_exh_prep<<<(ne + T - 1) / T, T, 0, st>>>(b, d_exh_ids, ne, d_feas, d_etbl, d_ecap);
+    out.launches++;
+    std::vector<long long> feas(nL, 0);
+    CK(cudaMemcpyAsync(feas.data(), d_feas, sizeof(long long) * nL, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    a.d2h_bytes += sizeof(long long) * nL;
+
+    // thread path: 1F1B with M >= P and P <= 8
+    std::vector<std::vector<hpk::ExhItem>> titems(9);
+    std::vector<std::vector<int>> tleaf(9);
+    std::vector<int> generic;
+    const long long per_item = 32LL * hpk::kExhChunk;
+    for (int k : exh_ids) {
+      const Leaf& lf = leaves[k];
+      if (feas[k] == 0) continue;
+      if (lf.sched == HP_1F1B && lf.M >= lf.P && lf.P <= 8) {
+        tleaf[lf.P].push_back(k);
+        for (long long r = 0; r < feas[k]; r += per_item)
+          titems[lf.P].push_back(hpk::ExhItem{k, 0, r, std::min(per_item, feas[k] - r)});
+      } else {
+        generic.push_back(k);
+      }
+    }
+    size_t nrec = 0;
+    for (int P = 1; P <= 8; ++P) nrec += titems[P].size();
+    if (nrec > 0) {
+      hpk::ExhRec* d_recs;
+      if (!(s = scratch(a, "exh_recs", nrec, &d_recs)).ok()) return s;
+      std::vector<int> mids, rb, re;
+      size_t off = 0;
+      for (int P = 1; P <= 8; ++P) {
+        if (titems[P].empty()) continue;
+        hpk::ExhItem* d_items;
+        std::string nm = "exh_items" + std::to_string(P);
+        if (!(s = upload(a, nm.c_str(), titems[P], &d_items)).ok()) return s;
+        const int ni = static_cast<int>(titems[P].size());
+        const int blocks = (ni * 32 + 127) / 128;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (a.time_evals) {
+          a.event_pair(&e0, &e1);
+          cudaEventRecord(e0, st);
+        }
+        switch (P) {
+          case 1: hpk::k_exh_thread<1><<<blocks, 128, 0, st>>>(b, d_items, ni, d_recs + off); break;
+          case 2: hpk::k_exh_thread<2><<<blocks, 128, 0, st>>>(b, d_items, ni, d_recs + off); break;
+          case 3: hpk::k_exh_thread<3><<<blocks, 128, 0, st>>>(b, d_items, ni, d_recs + off); break;
+          case 4: hpk::k_exh_thread<4><<<blocks, 128, 0, st>>>(b, d_items, ni, d_recs + off); break;
+          case 5: hpk::k_exh_thread<5><<<blocks, 128, 0, st>>>(b, d_items, ni, d_recs + off); break;
+          case 6: hpk::k_exh_thread<6><<<blocks, 128, 0, st>>>(b, d_items, ni, d_recs + off); break;
+          case 7: hpk::k_exh_thread<7><<<blocks, 128, 0, st>>>(b, d_items, ni, d_recs + off); break;
+          default: hpk::k_exh_thread<8><<<blocks, 128, 0, st>>>(b, d_items, ni, d_recs + off); break;
+        }
+        if (a.time_evals) cudaEventRecord(e1, st);
+        out.launches++;
+        out.eval_launches++;
+        // items of one leaf are contiguous
+        size_t j = 0;
+        while (j < titems[P].size()) {
+          int leaf = titems[P][j].leaf;
+          size_t j2 = j;
+          while (j2 < titems[P].size() && titems[P][j2].leaf == leaf) ++j2;
+          mids.push_back(leaf);
+          rb.push_back(static_cast<int>(off + j));
+          re.push_back(static_cast<int>(off + j2));
+          j = j2;
+        }
+        off += titems[P].size();
+      }
+      int *d_mids, *d_rb, *d_re;
+      if (!(s = upload(a, "exh_mids", mids, &d_mids)).ok()) return s;
+      if (!(s = upload(a, "exh_rb", rb, &d_rb)).ok()) return s;
+      if (!(s = upload(a, "exh_re", re, &d_re)).ok()) return s;
+      const int nm = static_cast<int>(mids.size());
+      hpk::k_exh_merge<<<(nm + T - 1) / T, T, 0, st>>>(b, d_recs, d_rb, d_re, d_mids, nm);
+      out.launches++;
+    }
+
+    // generic path: warp segments over bounded ranks, in chunks
+    if (!generic.empty()) {
+      const long long kChunk = 1 << 24;
+      double* d_x;
+      if (!(s = scratch(a, "xbuf", kChunk, &d_x)).ok()) return s;
+      b.xbuf = d_x;
+      size_t e = 0;
+      long long pos = 0;
+      while (e < generic.size()) {
+        std::vector<std::vector<Work>> q(hpk::NCLS);
+        std::vector<hpk::ExhSpan> spans;
+        long long used = 0;
+        while (e < generic.size() && used < kChunk) {
+          int k = generic[e];
+          const Leaf& lf = leaves[k];
+          long long total = feas[k];
+          long long take = std::min(total - pos, kChunk - used);
+          int cls = hpk::eval_class(lf.P, lf.M, lf.sched == 0);
+          int cpw = hpk::class_cpw(cls, lf.P);
+          for (long long j = 0; j < take; j += cpw)
+            q[cls].push_back(Work{k, 2, pos + j, (int)std::min<long long>(cpw, take - j), (int)(used + j), nullptr});
+          spans.push_back(hpk::ExhSpan{k, (int)used, pos, take});
+          used += take;
+          pos += take;
+          if (pos == total) {
+            ++e;
+            pos = 0;
+          }
+        }
+        if (!(s = run_queues(q, "exhq")).ok()) return s;
+        hpk::ExhSpan* d_spans;
+        if (!(s = upload(a, "spans", spans, &d_spans)).ok()) return s;
+        hpk::k_exh_reduce<<<((int)spans.size() + T - 1) / T, T, 0, st>>>(b, d_spans, (int)spans.size());
+        out.launches++;
+        CK(cudaStreamSynchronize(st));
+      }
+    }
+    hpk::k_exh_fix<<<(ne + T - 1) / T, T, 0, st>>>(b, d_exh_ids, ne, d_feas);
+    out.launches++;
   }
 
   // ---- final argmin

@@ -128,6 +128,95 @@ HPD bool split_enc_less(int P, const int* a, const int* b) {
   return false;
 }
 
+// ------------------------------------------------------------ exhaustive
+//
+// stage_memory (cost_model.cpp:75-86) is non-decreasing in the layer count
+// (every operation is monotone under round-to-nearest), so the memory gate
+// of evaluate_split (planner.cpp:502-517) accepts exactly the compositions
+// with count_i <= cap_i. The exhaustive regime therefore enumerates only the
+// bounded compositions, in the reference's lexicographic order restricted to
+// them, and counts the rest as memory-pruned analytically.
+
+// cap_i = largest count in [1, L] that passes stage i's memory gate, 0 if none.
+HPD void exh_caps(const Consts& c, const Leaf& lf, const LeafGroup* lg, const uint8_t* slots,
+                  int* caps) {
+  const int P = lf.P;
+  for (int i = 0; i < P; ++i) {
+    const LeafGroup& row = lg[slots[i]];
+    const double budget = c.budget[row.group];
+    const int inf = in_flight(c, i, P, lf.M);
+    int lo = 0, hi = c.L;  // invariant: lo passes (or 0), hi+1 fails
+    while (lo < hi) {
+      int mid = (lo + hi + 1) / 2;
+      double need = stage_memory(c, mid, row.tp, (double)lf.B, inf);
+      if (need > budget) hi = mid - 1;
+      else lo = mid;
+    }
+    caps[i] = lo;
+  }
+}
+
+// tbl[j*(L+1)+s] = number of compositions of s into stages j..P-1 with
+// 1 <= count_i <= cap_i (tbl[P][0] = 1). Returns tbl[0][L].
+HPD long long exh_table(int L, int P, const int* caps, long long* tbl) {
+  const int W = L + 1;
+  for (int s = 0; s <= L; ++s) tbl[P * W + s] = s == 0 ? 1 : 0;
+  for (int j = P - 1; j >= 0; --j) {
+    // tbl[j][s] = sum_{v=1..cap_j} tbl[j+1][s-v]  (sliding window)
+    long long run = 0;
+    for (int s = 0; s <= L; ++s) {
+      if (s - 1 >= 0) run += tbl[(j + 1) * W + s - 1];
+      if (s - 1 - caps[j] >= 0) run -= tbl[(j + 1) * W + s - 1 - caps[j]];
+      tbl[j * W + s] = caps[j] >= 1 ? run : 0;
+    }
+  }
+  return tbl[L];
+}
+
+// Bounded composition with lexicographic rank `rank` among the bounded ones.
+HPD void unrank_bounded(long long rank, int L, int P, const int* caps, const long long* tbl,
+                        int* out) {
+  const int W = L + 1;
+  int rem = L;
+  for (int j = 0; j < P - 1; ++j) {
+    for (int v = 1;; ++v) {
+      long long cnt = (v <= caps[j] && rem - v >= 0) ? tbl[(j + 1) * W + rem - v] : 0;
+      if (rank < cnt) {
+        out[j] = v;
+        rem -= v;
+        break;
+      }
+      rank -= cnt;
+    }
+  }
+  out[P - 1] = rem;
+}
+
+// Successor among the bounded compositions (false after the last one).
+// sufcap[j] = sum_{k>=j} caps[k].
+HPD bool next_bounded(int* c, int P, const int* caps, const int* sufcap) {
+  int suffix = c[P - 1];
+  for (int j = P - 2; j >= 0; --j) {
+    // parts j+1..P-1 sum to `suffix`; try c[j]+1 with suffix-1 left for them
+    const int rest = suffix - 1;
+    if (c[j] + 1 <= caps[j] && rest >= P - 1 - j && rest <= sufcap[j + 1]) {
+      c[j] += 1;
+      int r = rest;
+      for (int k = j + 1; k < P - 1; ++k) {
+        int need_after = sufcap[k + 1];  // most the later parts can take
+        int v = r - need_after;
+        if (v < 1) v = 1;
+        c[k] = v;
+        r -= v;
+      }
+      c[P - 1] = r;
+      return true;
+    }
+    suffix += c[j];
+  }
+  return false;
+}
+
 // ------------------------------------------------------------ hill climb
 
 // Per-leaf state of the steepest-descent search (planner.cpp:461-489) plus

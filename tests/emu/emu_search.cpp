@@ -155,3 +155,36 @@ extern "C" int emu_evaluate(const hp_problem* in, const hp_plan* plan, double* o
   *out = simulate_serial(c.schedule == 0 || plan->schedule == HP_GPIPE, P, lf.M, d.data(), ss.data());
   return 0;
 }
+
+// Bounded-composition machinery of the exhaustive regime: enumerates every
+// composition of L into P parts in lexicographic order (enumerate_splits,
+// planner.cpp:149-162), keeps those with count_i <= caps[i], and checks that
+// exh_table / unrank_bounded / next_bounded reproduce exactly that sequence.
+// Returns the number of bounded compositions, or -1 on a mismatch.
+extern "C" long long emu_check_bounded(int L, int P, const int* caps) {
+  std::vector<long long> tbl((size_t)(P + 1) * (L + 1));
+  long long F = exh_table(L, P, caps, tbl.data());
+  std::vector<int> sufcap(P + 1, 0);
+  for (int j = P - 1; j >= 0; --j) sufcap[j] = sufcap[j + 1] + caps[j];
+  std::vector<int> comp(P), want(P), got(P);
+  long long n = 0;
+  bool have_iter = false;
+  unrank_composition(0, L, P, comp.data());
+  do {
+    bool ok = true;
+    for (int i = 0; i < P; ++i) ok = ok && comp[i] <= caps[i];
+    if (!ok) continue;
+    unrank_bounded(n, L, P, caps, tbl.data(), got.data());
+    if (got != comp) return -1;
+    if (!have_iter) {
+      want = comp;
+      have_iter = true;
+    } else {
+      if (!next_bounded(want.data(), P, caps, sufcap.data())) return -1;
+      if (want != comp) return -1;
+    }
+    ++n;
+  } while (next_composition(comp.data(), P));
+  if (have_iter && next_bounded(want.data(), P, caps, sufcap.data())) return -1;
+  return n == F ? n : -1;
+}

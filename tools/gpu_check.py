@@ -66,3 +66,12 @@ if which in ("default",):
         if not line["match"]:
             line["ref"] = [rr["candidates_simulated"], rr["candidates_pruned"], rr["eval"]["iteration_time_s"], renc, enc]
         print(json.dumps(line), flush=True)
+if which in ("c5",):
+    c = configs.config("C5"); c["model"]["num_layers"] = 40
+    run("C5-L40", c)
+    c = configs.config("C5"); c["model"]["num_layers"] = 40; c["planner"]["schedule"] = "gpipe"
+    for g in c["cluster"]["groups"]: g["memory_bytes"] = 400e9
+    run("C5-L40-gpipe", c)
+    c = configs.config("C5"); c["planner"]["pipeline_degrees"] = [3]; c["planner"]["micro_batch_candidates"] = [1]
+    run("C5pp3B1", c, check=False)
+    run("C5", configs.config("C5"), check=False, timed=True)
