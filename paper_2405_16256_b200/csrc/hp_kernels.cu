@@ -331,7 +331,9 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
   const double* hop = b.hop + lf.B_idx * c_consts.n_links;
   const double NEG = -__longlong_as_double(0x7ff0000000000000LL) * 1.0;  // -inf
 
-  double f[K], bw[K], sf[K], sb[K], dps[K];
+  // per stage: durations and forward hop; the backward hop of stage i is
+  // the forward hop of stage i-1 (same link and volume, evaluate.cpp:59-62)
+  double f[K], bw[K], sf[K];
   bool valid = true, mem_ok = true;
   int cnt[K];
   if (w.kind == 2 && has_cand) {
@@ -359,10 +361,10 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
   for (int r = 0; r < K; ++r) {
     const int i = sl * K + r;
     f[r] = bw[r] = NEG;
-    sf[r] = sb[r] = 0.0;
-    dps[r] = 0.0;
+    sf[r] = 0.0;
     if (has_cand && i < P) {
       int c = w.kind == 2 ? cnt[r] : cand_count(b, lf, w, seg, i);
+      cnt[r] = c;
       StageDur d;
       if (c < 1) {
         valid = false;
@@ -375,8 +377,6 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
         // channels at -inf, which doubles as the "no dependency" operand for
         // the neighbouring segment / padding lanes (max(x, -inf) = x).
         sf[r] = i == P - 1 ? NEG : d.sf;
-        sb[r] = i == 0 ? NEG : d.sb;
-        dps[r] = d.dps;
       }
     }
   }
@@ -394,7 +394,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
     const bool real = run && i < P;
     if (!real) {
       f[r] = bw[r] = NEG;
-      sf[r] = sb[r] = 0.0;
+      sf[r] = 0.0;
     }
     fr[r] = real ? 0.0 : NEG;
     chf[r] = (real && i != P - 1) ? 0.0 : NEG;
@@ -402,6 +402,9 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
   }
   const int src_l = (lane + 31) & 31;   // rotate: lane 0 reads lane 31 (-inf)
   const int src_r = (lane + 1) & 31;
+  // backward hop of the lane's first stage; stage 0 sends no gradient (-inf)
+  const double sb_in = __shfl_sync(0xffffffffu, sf[K - 1], src_l);
+  const double sb0 = sl == 0 ? NEG : sb_in;
   if (__any_sync(0xffffffffu, run)) {
     // ---- warm-up, levels 0..P-1: stage i runs F(i, t-i) once t >= i
     for (int t = 0; t < P; ++t) {
@@ -450,7 +453,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
         } else {
           const double recv = r == K - 1 ? rchb : chb[r < K - 1 ? r + 1 : 0];
           const double nfr = dmax(fr[r], recv) + bw[r];
-          const double nch = dmax(nfr, chb[r]) + sb[r];
+          const double nch = dmax(nfr, chb[r]) + (r == 0 ? sb0 : sf[r > 0 ? r - 1 : 0]);
           if (PRED) {
             // B(i,j) at level 2P-1-i+2j: 2P-1-i <= t <= 2M+2P-3-i
             const bool act = (u0 + r >= 2 * P - 1) && (u0 + r <= 2 * M + 2 * P - 3);
@@ -494,7 +497,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
       v = dmax(v, fr[r]);
       v = dmax(v, chf[r]);
       v = dmax(v, chb[r]);
-      v = dmax(v, fr[r] + dps[r]);
+      v = dmax(v, fr[r] + dp_sync(lg[slots[i]], cnt[r]));
     }
   }
   for (int off = 1; off < W; off <<= 1) {
@@ -1349,6 +1352,12 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     int cpw = hpk::class_cpw(cls, leaves[k].P);
     items_cls[cls] += (2 * (leaves[k].P - 1) + cpw - 1) / cpw;
   }
+  // Longest steps first: the seeding order is the initial queue order, so
+  // the slowest leaves start early instead of forming the tail.
+  for (auto& v : by_cls)
+    std::stable_sort(v.begin(), v.end(), [&](int x, int y) {
+      return (double)leaves[x].M * leaves[x].P > (double)leaves[y].M * leaves[y].P;
+    });
   size_t qcap = 1024;
   for (int cls = 0; cls < hpk::NCLS; ++cls) qcap = std::max(qcap, items_cls[cls] + 1024);
   hpk::AsyncQ q{};
