@@ -260,7 +260,11 @@ def main_ours(args):
     vec = torch.tensor([sum(dev_ms) / len(dev_ms), sum(wall_ms) / len(wall_ms)], dtype=torch.float64,
                        device="cuda")
     agg = torch.tensor([h2d, d2h, float(launches), eval_ms, eval_ops], dtype=torch.float64, device="cuda")
+    per_rank = [float(vec[0])]
     if world > 1:
+        allv = torch.empty(world * 2, dtype=torch.float64, device="cuda")
+        dist.all_gather_into_tensor(allv, vec)
+        per_rank = [float(x) for x in allv[0::2].cpu()]
         dist.all_reduce(vec, op=dist.ReduceOp.MAX)
         dist.all_reduce(agg, op=dist.ReduceOp.SUM)
     dev_step_ms, wall_step_ms = float(vec[0]), float(vec[1])
@@ -296,6 +300,7 @@ def main_ours(args):
                    "best_iteration_time_s": red.best_time_s,
                    "best_plan": abi.encode_plan(problem.group_names, red.best_plan),
                    "parallelism": f"leaf-sharded x{world}",
+                   "rank_device_ms": per_rank,
                    "l2": "flushed between timed steps (256 MiB write); per-step inputs are KB-sized tables"},
         "e2e": {"value": cands / (wall_step_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
