@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -541,24 +542,33 @@ __global__ void __launch_bounds__(256) k_eval(Bufs b, const Work* items, const i
 // a leaf runs that leaf's step (hill_step) and enqueues its next neighbours,
 // so there is no global per-step barrier and no host round trip; the kernel
 // ends when no leaf of its class is still climbing.
+// Two FIFO rings with ticket claims: level 0 (priority) receives the steps
+// of leaves that have already made kHiSteps moves — long climbers are the
+// critical path of a class, so their items should not wait behind a full
+// round of every other leaf's items — level 1 everything else. Each warp
+// holds at most one ticket per ring; it claims a priority ticket only when
+// the priority ring has unclaimed items, serves whichever of its tickets is
+// filled first, and keeps them across items (no CAS loops, no contention).
+constexpr int kHiSteps = 8;
+
 struct AsyncQ {
-  Work* slots;
-  unsigned long long* seq;   // slot k holds ticket t when seq[k] == t + 1
-  unsigned long long* head;  // next ticket to consume
-  unsigned long long* tail;  // next ticket to produce
-  int* pending;              // per leaf: items of the current step not yet done
-  int* active;               // leaves of this class still climbing
-  int* abort;                // watchdog flag
+  Work* slots[2];
+  unsigned long long* seq[2];   // slot k holds ticket t when seq[k] == t + 1
+  unsigned long long* head[2];  // next ticket to hand out
+  unsigned long long* tail[2];  // next ticket to produce
+  int* pending;                 // per leaf: items of the current step not yet done
+  int* active;                  // leaves of this class still climbing
+  int* abort;                   // watchdog flag
   unsigned long long cap;
 };
 
-__device__ void push_items(const Bufs& b, const AsyncQ& q, int li, int cls) {
+__device__ void push_items(const Bufs& b, const AsyncQ& q, int li, int cls, int level) {
   const Leaf lf = b.leaves[li];
   const int cpw = class_cpw(cls, lf.P);
   const int nslots = 2 * (lf.P - 1);
   const int nit = (nslots + cpw - 1) / cpw;
   q.pending[li] = nit;
-  unsigned long long t = atomicAdd(q.tail, (unsigned long long)nit);
+  unsigned long long t = atomicAdd(q.tail[level], (unsigned long long)nit);
   for (int j = 0; j < nit; ++j) {
     Work w;
     w.leaf = li;
@@ -568,9 +578,9 @@ __device__ void push_items(const Bufs& b, const AsyncQ& q, int li, int cls) {
     w.out = 0;
     w.ids = nullptr;
     const unsigned long long k = (t + j) % q.cap;
-    q.slots[k] = w;
+    q.slots[level][k] = w;
     __threadfence();
-    atomicExch(q.seq + k, t + j + 1);
+    atomicExch(q.seq[level] + k, t + j + 1);
   }
 }
 
@@ -581,46 +591,53 @@ __global__ void k_async_seed(Bufs b, AsyncQ q, const int* ids, int n, int cls) {
   int li = ids[k];
   if (!b.hs[li].active) return;
   atomicAdd(q.active, 1);
-  push_items(b, q, li, cls);
+  push_items(b, q, li, cls, 1);
+}
+
+__device__ __forceinline__ bool try_slot(const AsyncQ& q, int lv, long long& ticket, Work& w) {
+  const unsigned long long h = (unsigned long long)ticket;
+  const unsigned long long k = h % q.cap;
+  if (*(volatile unsigned long long*)(q.seq[lv] + k) != h + 1) return false;
+  __threadfence();
+  const Work* sl = q.slots[lv] + k;
+  w.leaf = __ldcg(&sl->leaf);
+  w.kind = __ldcg(&sl->kind);
+  w.first = __ldcg(&sl->first);
+  w.n = __ldcg(&sl->n);
+  ticket = -1;
+  return true;
+}
+
+// Lane 0: next item for this warp (see AsyncQ). Returns false when the class
+// is finished or aborted.
+__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[2]) {
+  unsigned ns = 32;
+  const long long t0 = clock64();
+  for (;;) {
+    if (tk[0] < 0 && *(volatile unsigned long long*)q.tail[0] > *(volatile unsigned long long*)q.head[0])
+      tk[0] = (long long)atomicAdd(q.head[0], 1ULL);
+    if (tk[0] >= 0 && try_slot(q, 0, tk[0], w)) return true;
+    if (tk[1] < 0) tk[1] = (long long)atomicAdd(q.head[1], 1ULL);
+    if (try_slot(q, 1, tk[1], w)) return true;
+    if (*(volatile int*)q.active == 0 || *(volatile int*)q.abort) return false;
+    // watchdog: ~30 s without work while leaves are active means a bug
+    if (clock64() - t0 > (1LL << 36)) {
+      atomicExch(q.abort, 1);
+      return false;
+    }
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+  }
 }
 
 template <int K, bool FAST>
 __global__ void __launch_bounds__(256) k_hill_async(Bufs b, AsyncQ q, int cls) {
   const int lane = threadIdx.x & 31;
+  long long tk[2] = {-1, -1};
   for (;;) {
-    unsigned long long h = 0;
     int quit = 0;
     Work w{};
-    if (lane == 0) {
-      h = atomicAdd(q.head, 1ULL);
-      const unsigned long long k = h % q.cap;
-      volatile unsigned long long* sq = q.seq + k;
-      unsigned ns = 32;
-      const long long t0 = clock64();
-      while (*sq != h + 1) {
-        if (*(volatile int*)q.active == 0 || *(volatile int*)q.abort) {
-          quit = 1;
-          break;
-        }
-        // watchdog: a queue that stalls for ~30 s means a bookkeeping bug;
-        // abort instead of hanging the GPU (reported as HP_INTERNAL)
-        if (clock64() - t0 > (1LL << 36)) {
-          atomicExch(q.abort, 1);
-          quit = 1;
-          break;
-        }
-        __nanosleep(ns);
-        if (ns < 2048) ns <<= 1;
-      }
-      if (!quit) {
-        __threadfence();
-        const Work* s = q.slots + k;
-        w.leaf = __ldcg(&s->leaf);
-        w.kind = __ldcg(&s->kind);
-        w.first = __ldcg(&s->first);
-        w.n = __ldcg(&s->n);
-      }
-    }
+    if (lane == 0) quit = pop_item(q, w, tk) ? 0 : 1;
     quit = __shfl_sync(0xffffffffu, quit, 0);
     if (quit) return;
     w.leaf = __shfl_sync(0xffffffffu, w.leaf, 0);
@@ -648,7 +665,7 @@ __global__ void __launch_bounds__(256) k_hill_async(Bufs b, AsyncQ q, int cls) {
         b.hs[li] = hs;
         if (hs.active) {
           __threadfence();
-          push_items(b, q, li, cls);
+          push_items(b, q, li, cls, hs.steps >= kHiSteps ? 0 : 1);
         } else {
           __threadfence();
           atomicSub(q.active, 1);
@@ -1361,17 +1378,23 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   size_t qcap = 1024;
   for (int cls = 0; cls < hpk::NCLS; ++cls) qcap = std::max(qcap, items_cls[cls] + 1024);
   hpk::AsyncQ q{};
-  if (!(s = scratch(a, "q_slots", qcap, &q.slots)).ok()) return s;
-  if (!(s = scratch(a, "q_seq", qcap, &q.seq)).ok()) return s;
+  for (int lv = 0; lv < 2; ++lv) {
+    std::string nm = "q_slots" + std::to_string(lv);
+    if (!(s = scratch(a, nm.c_str(), qcap, &q.slots[lv])).ok()) return s;
+    nm = "q_seq" + std::to_string(lv);
+    if (!(s = scratch(a, nm.c_str(), qcap, &q.seq[lv])).ok()) return s;
+  }
   unsigned long long* d_q;
-  if (!(s = scratch(a, "q_ctr", 4, &d_q)).ok()) return s;
+  if (!(s = scratch(a, "q_ctr", 8, &d_q)).ok()) return s;
   int* d_pending;
   if (!(s = scratch(a, "q_pending", nL, &d_pending)).ok()) return s;
-  q.head = d_q;
-  q.tail = d_q + 1;
-  q.active = reinterpret_cast<int*>(d_q + 2);
-  q.abort = reinterpret_cast<int*>(d_q + 3);
-  CK(cudaMemsetAsync(d_q, 0, sizeof(unsigned long long) * 4, st));
+  q.head[0] = d_q;
+  q.head[1] = d_q + 1;
+  q.tail[0] = d_q + 2;
+  q.tail[1] = d_q + 3;
+  q.active = reinterpret_cast<int*>(d_q + 4);
+  q.abort = reinterpret_cast<int*>(d_q + 5);
+  CK(cudaMemsetAsync(d_q, 0, sizeof(unsigned long long) * 8, st));
   q.pending = d_pending;
   q.cap = qcap;
   for (int cls = 0; cls < hpk::NCLS; ++cls) {
@@ -1379,8 +1402,9 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     int* d_cls_ids;
     std::string nm = "cls_ids" + std::to_string(cls);
     if (!(s = upload(a, nm.c_str(), by_cls[cls], &d_cls_ids)).ok()) return s;
-    CK(cudaMemsetAsync(q.seq, 0, sizeof(unsigned long long) * qcap, st));
-    CK(cudaMemsetAsync(d_q, 0, sizeof(unsigned long long) * 3, st));
+    CK(cudaMemsetAsync(q.seq[0], 0, sizeof(unsigned long long) * qcap, st));
+    CK(cudaMemsetAsync(q.seq[1], 0, sizeof(unsigned long long) * qcap, st));
+    CK(cudaMemsetAsync(d_q, 0, sizeof(unsigned long long) * 5, st));
     int n = static_cast<int>(by_cls[cls].size());
     hpk::k_async_seed<<<(n + T - 1) / T, T, 0, st>>>(b, q, d_cls_ids, n, cls);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1392,6 +1416,12 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     if (a.time_evals) cudaEventRecord(e1, st);
     out.launches += 2;
     out.eval_launches++;
+    if (std::getenv("HP_DEBUG_TIMING") && e1) {
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      std::fprintf(stderr, "[hp] class %d: %d leaves, %.2f ms\n", cls, n, ms);
+    }
   }
   out.hill_iterations = 0;
   if (!by_cls.empty()) {
