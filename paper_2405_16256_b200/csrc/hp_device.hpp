@@ -18,6 +18,29 @@ struct Arena {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   std::map<std::string, std::pair<void*, size_t>> bufs;
+  // side streams (one per evaluator class, created on first use) and a pool
+  // of ordering events
+  cudaStream_t sides[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> markers;
+  size_t markers_used = 0;
+
+  cudaStream_t side(int k) {
+    if (!sides[k]) cudaStreamCreateWithFlags(&sides[k], cudaStreamNonBlocking);
+    return sides[k];
+  }
+
+  // An event for stream ordering; recycled after 256 uses (callers
+  // synchronise long before that).
+  cudaEvent_t marker() {
+    if (markers.size() < 256) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      markers.push_back(e);
+      return e;
+    }
+    return markers[markers_used++ % markers.size()];
+  }
+
   // optional per-launch timing of the evaluator kernels (bench roofline)
   bool time_evals = false;
   double h2d_bytes = 0.0, d2h_bytes = 0.0;  // per search
@@ -67,6 +90,13 @@ struct Arena {
     bufs.clear();
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     ev_pool.clear();
+    for (cudaEvent_t e : markers) cudaEventDestroy(e);
+    markers.clear();
+    for (cudaStream_t& s : sides)
+      if (s) {
+        cudaStreamDestroy(s);
+        s = nullptr;
+      }
   }
 };
 

@@ -82,6 +82,7 @@ struct Bufs {
   unsigned long long* ops;  // algorithmic FP64 add/max ops of simulated candidates
   // exhaustive regime: per-leaf bounded-composition tables (exh_table) and
   // memory caps; ranks of kind-2 work items index the bounded compositions
+  unsigned long long* trace;  // optional (HP_DEBUG_TRACE): [0] = count, then per-step (ns, leaf)
   const long long* etbl;
   const int* etbl_off;
   const int* ecap;
@@ -558,7 +559,8 @@ struct AsyncQ {
   unsigned long long* tail[2];  // next ticket to produce
   int* pending;                 // per leaf: items of the current step not yet done
   int* active;                  // leaves of this class still climbing
-  int* abort;                   // watchdog flag
+  int* abort;                   // watchdog flag (shared by all classes)
+  int* live;                    // resident warps of this class's kernel
   unsigned long long cap;
 };
 
@@ -608,18 +610,30 @@ __device__ __forceinline__ bool try_slot(const AsyncQ& q, int lv, long long& tic
   return true;
 }
 
-// Lane 0: next item for this warp (see AsyncQ). Returns false when the class
-// is finished or aborted.
+// Lane 0: next item for this warp (see AsyncQ). Tickets are claimed only
+// when the ring shows unclaimed items, so an idle warp holds none and may
+// retire: in the tail of a class (few leaves left), surplus idle warps exit
+// and free their SM for the next class's kernel, launched concurrently on
+// another stream. At least 64 warps per climbing leaf stay resident.
+// Returns false when the warp should exit.
 __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[2]) {
   unsigned ns = 32;
   const long long t0 = clock64();
+  int idle = 0;
   for (;;) {
-    if (tk[0] < 0 && *(volatile unsigned long long*)q.tail[0] > *(volatile unsigned long long*)q.head[0])
-      tk[0] = (long long)atomicAdd(q.head[0], 1ULL);
-    if (tk[0] >= 0 && try_slot(q, 0, tk[0], w)) return true;
-    if (tk[1] < 0) tk[1] = (long long)atomicAdd(q.head[1], 1ULL);
-    if (try_slot(q, 1, tk[1], w)) return true;
-    if (*(volatile int*)q.active == 0 || *(volatile int*)q.abort) return false;
+#pragma unroll
+    for (int lv = 0; lv < 2; ++lv) {
+      if (tk[lv] < 0 &&
+          *(volatile unsigned long long*)q.tail[lv] > *(volatile unsigned long long*)q.head[lv])
+        tk[lv] = (long long)atomicAdd(q.head[lv], 1ULL);
+      if (tk[lv] >= 0 && try_slot(q, lv, tk[lv], w)) return true;
+    }
+    const int act = *(volatile int*)q.active;
+    if (act == 0 || *(volatile int*)q.abort) return false;
+    if (tk[0] < 0 && tk[1] < 0 && ++idle > 8 && act * 64 < *(volatile int*)q.live) {
+      if (atomicSub(q.live, 1) > act * 64) return false;
+      atomicAdd(q.live, 1);
+    }
     // watchdog: ~30 s without work while leaves are active means a bug
     if (clock64() - t0 > (1LL << 36)) {
       atomicExch(q.abort, 1);
@@ -663,6 +677,16 @@ __global__ void __launch_bounds__(256) k_hill_async(Bufs b, AsyncQ q, int cls) {
                   b.uni + lf.split_off, b.prop + lf.split_off, b.best + lf.split_off,
                   b.hist + b.hist_off[li], hs, b.nb + b.nb_off[li], delta, old, tmp);
         b.hs[li] = hs;
+        if (b.trace) {
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          unsigned long long k = atomicAdd(b.trace, 1ULL);
+          if (k < (1ULL << 22)) {
+            b.trace[1 + 2 * k] = now;
+            b.trace[2 + 2 * k] = ((unsigned long long)cls << 56) | ((unsigned long long)lf.P << 40) |
+                                 ((unsigned long long)lf.M << 24) | (unsigned)(li & 0xffffff);
+          }
+        }
         if (hs.active) {
           __threadfence();
           push_items(b, q, li, cls, hs.steps >= kHiSteps ? 0 : 1);
@@ -1180,17 +1204,30 @@ static int async_grid(int sm_count) {
   return sm_count * (per_sm > 0 ? per_sm : 1);
 }
 
-static void launch_async(int cls, const hpk::Bufs& b, const hpk::AsyncQ& q, int sm_count,
+static int async_grid_of(int cls, int sm_count) {
+  switch (cls) {
+    case 0: return async_grid<2, true>(sm_count);
+    case 1: return async_grid<4, true>(sm_count);
+    case 2: return async_grid<6, true>(sm_count);
+    case 3: return async_grid<8, true>(sm_count);
+    case 4: return async_grid<1, false>(sm_count);
+    case 5: return async_grid<2, false>(sm_count);
+    case 6: return async_grid<3, false>(sm_count);
+    default: return async_grid<8, false>(sm_count);
+  }
+}
+
+static void launch_async(int cls, const hpk::Bufs& b, const hpk::AsyncQ& q, int grid,
                          cudaStream_t st) {
   switch (cls) {
-    case 0: hpk::k_hill_async<2, true><<<async_grid<2, true>(sm_count), 256, 0, st>>>(b, q, cls); break;
-    case 1: hpk::k_hill_async<4, true><<<async_grid<4, true>(sm_count), 256, 0, st>>>(b, q, cls); break;
-    case 2: hpk::k_hill_async<6, true><<<async_grid<6, true>(sm_count), 256, 0, st>>>(b, q, cls); break;
-    case 3: hpk::k_hill_async<8, true><<<async_grid<8, true>(sm_count), 256, 0, st>>>(b, q, cls); break;
-    case 4: hpk::k_hill_async<1, false><<<async_grid<1, false>(sm_count), 256, 0, st>>>(b, q, cls); break;
-    case 5: hpk::k_hill_async<2, false><<<async_grid<2, false>(sm_count), 256, 0, st>>>(b, q, cls); break;
-    case 6: hpk::k_hill_async<3, false><<<async_grid<3, false>(sm_count), 256, 0, st>>>(b, q, cls); break;
-    default: hpk::k_hill_async<8, false><<<async_grid<8, false>(sm_count), 256, 0, st>>>(b, q, cls); break;
+    case 0: hpk::k_hill_async<2, true><<<grid, 256, 0, st>>>(b, q, cls); break;
+    case 1: hpk::k_hill_async<4, true><<<grid, 256, 0, st>>>(b, q, cls); break;
+    case 2: hpk::k_hill_async<6, true><<<grid, 256, 0, st>>>(b, q, cls); break;
+    case 3: hpk::k_hill_async<8, true><<<grid, 256, 0, st>>>(b, q, cls); break;
+    case 4: hpk::k_hill_async<1, false><<<grid, 256, 0, st>>>(b, q, cls); break;
+    case 5: hpk::k_hill_async<2, false><<<grid, 256, 0, st>>>(b, q, cls); break;
+    case 6: hpk::k_hill_async<3, false><<<grid, 256, 0, st>>>(b, q, cls); break;
+    default: hpk::k_hill_async<8, false><<<grid, 256, 0, st>>>(b, q, cls); break;
   }
 }
 
@@ -1377,53 +1414,99 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     });
   size_t qcap = 1024;
   for (int cls = 0; cls < hpk::NCLS; ++cls) qcap = std::max(qcap, items_cls[cls] + 1024);
-  hpk::AsyncQ q{};
-  for (int lv = 0; lv < 2; ++lv) {
-    std::string nm = "q_slots" + std::to_string(lv);
-    if (!(s = scratch(a, nm.c_str(), qcap, &q.slots[lv])).ok()) return s;
-    nm = "q_seq" + std::to_string(lv);
-    if (!(s = scratch(a, nm.c_str(), qcap, &q.seq[lv])).ok()) return s;
+  if (std::getenv("HP_DEBUG_TRACE")) {
+    if (!(s = scratch(a, "trace", 1 + 2 * (1ULL << 22), &b.trace)).ok()) return s;
+    CK(cudaMemsetAsync(b.trace, 0, sizeof(unsigned long long), st));
   }
-  unsigned long long* d_q;
-  if (!(s = scratch(a, "q_ctr", 8, &d_q)).ok()) return s;
+  // One queue per class; the class kernels run concurrently on side streams,
+  // largest class first, and retire idle warps in their tails (pop_item) so
+  // the next class fills the freed SMs.
   int* d_pending;
   if (!(s = scratch(a, "q_pending", nL, &d_pending)).ok()) return s;
-  q.head[0] = d_q;
-  q.head[1] = d_q + 1;
-  q.tail[0] = d_q + 2;
-  q.tail[1] = d_q + 3;
-  q.active = reinterpret_cast<int*>(d_q + 4);
-  q.abort = reinterpret_cast<int*>(d_q + 5);
-  CK(cudaMemsetAsync(d_q, 0, sizeof(unsigned long long) * 8, st));
-  q.pending = d_pending;
-  q.cap = qcap;
+  int* d_abort;
+  if (!(s = scratch(a, "q_abort", 1, &d_abort)).ok()) return s;
+  CK(cudaMemsetAsync(d_abort, 0, sizeof(int), st));
+  std::vector<int> order;
+  std::vector<double> cls_cost(hpk::NCLS, 0.0);
   for (int cls = 0; cls < hpk::NCLS; ++cls) {
-    if (by_cls[cls].empty()) continue;
-    int* d_cls_ids;
+    for (int k : by_cls[cls]) cls_cost[cls] += (double)leaves[k].M * leaves[k].P * leaves[k].P;
+    if (!by_cls[cls].empty()) order.push_back(cls);
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cls_cost[x] > cls_cost[y]; });
+  // class id lists go up on the main stream before the side streams fork
+  std::vector<int*> d_cls_ids(hpk::NCLS, nullptr);
+  for (int cls : order) {
     std::string nm = "cls_ids" + std::to_string(cls);
-    if (!(s = upload(a, nm.c_str(), by_cls[cls], &d_cls_ids)).ok()) return s;
-    CK(cudaMemsetAsync(q.seq[0], 0, sizeof(unsigned long long) * qcap, st));
-    CK(cudaMemsetAsync(q.seq[1], 0, sizeof(unsigned long long) * qcap, st));
-    CK(cudaMemsetAsync(d_q, 0, sizeof(unsigned long long) * 5, st));
-    int n = static_cast<int>(by_cls[cls].size());
-    hpk::k_async_seed<<<(n + T - 1) / T, T, 0, st>>>(b, q, d_cls_ids, n, cls);
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (a.time_evals) {
-      a.event_pair(&e0, &e1);
-      cudaEventRecord(e0, st);
+    if (!(s = upload(a, nm.c_str(), by_cls[cls], &d_cls_ids[cls])).ok()) return s;
+  }
+  cudaEvent_t ready = a.marker();
+  cudaEvent_t h0 = nullptr, h1 = nullptr;  // the concurrent class kernels as one timed region
+  if (a.time_evals && !order.empty()) {
+    a.event_pair(&h0, &h1);
+    CK(cudaEventRecord(h0, st));
+  }
+  CK(cudaEventRecord(ready, st));
+  std::vector<hpk::AsyncQ> qs(hpk::NCLS);
+  for (int cls : order) {
+    cudaStream_t ss = a.side(cls);
+    CK(cudaStreamWaitEvent(ss, ready, 0));
+    hpk::AsyncQ& q = qs[cls];
+    const size_t qcap = items_cls[cls] + 1024;
+    for (int lv = 0; lv < 2; ++lv) {
+      std::string nm = "q_slots" + std::to_string(cls) + "_" + std::to_string(lv);
+      if (!(s = scratch(a, nm.c_str(), qcap, &q.slots[lv])).ok()) return s;
+      nm = "q_seq" + std::to_string(cls) + "_" + std::to_string(lv);
+      if (!(s = scratch(a, nm.c_str(), qcap, &q.seq[lv])).ok()) return s;
+      CK(cudaMemsetAsync(q.seq[lv], 0, sizeof(unsigned long long) * qcap, ss));
     }
-    launch_async(cls, b, q, a.sm_count, st);
-    if (a.time_evals) cudaEventRecord(e1, st);
+    unsigned long long* d_q;
+    std::string nm = "q_ctr" + std::to_string(cls);
+    if (!(s = scratch(a, nm.c_str(), 8, &d_q)).ok()) return s;
+    q.head[0] = d_q;
+    q.head[1] = d_q + 1;
+    q.tail[0] = d_q + 2;
+    q.tail[1] = d_q + 3;
+    q.active = reinterpret_cast<int*>(d_q + 4);
+    q.live = reinterpret_cast<int*>(d_q + 5);
+    q.abort = d_abort;
+    q.pending = d_pending;
+    q.cap = qcap;
+    const int grid = async_grid_of(cls, a.sm_count);
+    unsigned long long init[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    reinterpret_cast<int*>(init + 5)[0] = grid * 8;  // warps of the launch
+    CK(cudaMemcpyAsync(d_q, init, sizeof init, cudaMemcpyHostToDevice, ss));
+    int n = static_cast<int>(by_cls[cls].size());
+    hpk::k_async_seed<<<(n + T - 1) / T, T, 0, ss>>>(b, q, d_cls_ids[cls], n, cls);
+    launch_async(cls, b, q, grid, ss);
     out.launches += 2;
     out.eval_launches++;
-    if (std::getenv("HP_DEBUG_TIMING") && e1) {
-      cudaEventSynchronize(e1);
-      float ms = 0;
-      cudaEventElapsedTime(&ms, e0, e1);
-      std::fprintf(stderr, "[hp] class %d: %d leaves, %.2f ms\n", cls, n, ms);
+  }
+  for (int cls : order) {
+    cudaEvent_t done = a.marker();
+    CK(cudaEventRecord(done, a.side(cls)));
+    CK(cudaStreamWaitEvent(st, done, 0));
+  }
+  if (h1) CK(cudaEventRecord(h1, st));
+  // the pinned init blocks above must outlive their copies
+  CK(cudaStreamSynchronize(st));
+  if (std::getenv("HP_DEBUG_TIMING") && a.time_evals) {
+    std::fprintf(stderr, "[hp] classes launched concurrently: %zu\n", order.size());
+  }
+  hpk::AsyncQ q = order.empty() ? hpk::AsyncQ{} : qs[order[0]];
+  q.abort = d_abort;
+  out.hill_iterations = 0;
+  if (b.trace) {
+    CK(cudaStreamSynchronize(st));
+    unsigned long long n = 0;
+    CK(cudaMemcpy(&n, b.trace, sizeof n, cudaMemcpyDeviceToHost));
+    n = std::min<unsigned long long>(n, 1ULL << 22);
+    std::vector<unsigned long long> tr(2 * n);
+    CK(cudaMemcpy(tr.data(), b.trace + 1, sizeof(unsigned long long) * 2 * n, cudaMemcpyDeviceToHost));
+    if (FILE* fp = std::fopen(std::getenv("HP_DEBUG_TRACE"), "wb")) {
+      std::fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fp);
+      std::fclose(fp);
     }
   }
-  out.hill_iterations = 0;
   if (!by_cls.empty()) {
     int abort_flag = 0;
     CK(cudaMemcpyAsync(&abort_flag, q.abort, sizeof(int), cudaMemcpyDeviceToHost, st));
