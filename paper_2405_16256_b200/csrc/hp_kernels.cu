@@ -683,8 +683,10 @@ __global__ void __launch_bounds__(256) k_hill_async(Bufs b, AsyncQ q, int cls) {
           unsigned long long k = atomicAdd(b.trace, 1ULL);
           if (k < (1ULL << 22)) {
             b.trace[1 + 2 * k] = now;
-            b.trace[2 + 2 * k] = ((unsigned long long)cls << 56) | ((unsigned long long)lf.P << 40) |
-                                 ((unsigned long long)lf.M << 24) | (unsigned)(li & 0xffffff);
+            const unsigned long long mv = hs.steps > 0 ? (unsigned)b.hist[b.hist_off[li] + hs.steps - 1] : 0xfff;
+            b.trace[2 + 2 * k] = ((unsigned long long)cls << 56) | ((unsigned long long)(lf.P & 0xff) << 48) |
+                                 ((unsigned long long)(lf.M & 0xffff) << 32) | ((mv & 0xfff) << 20) |
+                                 (unsigned)(li & 0xfffff);
           }
         }
         if (hs.active) {
