@@ -7,8 +7,8 @@
  *    implementation planner.cpp:579-685).
  * The reference exposes no FFI; this header is the flat, exception-free
  * equivalent (plain structs, pointers and sizes, no C++/torch types). The C++
- * mirror with the reference's exact signature lives in hetplan_b200.hpp and is
- * implemented over these entry points.
+ * function with the reference's exact signature is implemented over these
+ * entry points in integration/hetplan_search_b200.cpp.
  *
  * Every entry point returns an hp_status; on failure hp_last_error(ctx) holds a
  * message. Status codes follow the reference's exception kinds
@@ -152,6 +152,8 @@ typedef struct hp_plan {
  * sharded search passes the min over shards of hp_probe() in global_bound
  * with have_global_bound = 1. */
 #define HP_FLAG_TIME_KERNELS 1 /* time every evaluator launch with CUDA events */
+#define HP_FLAG_LOG 2          /* record the search log (SearchOutcome::log), read it
+                                  back with hp_search_log() */
 
 typedef struct hp_search_opts {
   int32_t shard_index;
@@ -221,6 +223,30 @@ hp_status hp_probe(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts*
  * caller decides infeasibility after reducing over shards. */
 hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts* opts,
                     hp_result* result);
+
+/* One SearchLogEntry (planner.hpp:95-99). The reference appends one per
+ * candidate it decides, in task order and, inside a task, in visit order
+ * (planner.cpp:306-551, 656-660); memo hits are not logged. Strings live in
+ * the text buffer of hp_search_log as NUL-terminated UTF-8 and are
+ * byte-identical to the reference's: `candidate` is the compact JSON
+ * descriptor (nlohmann dump, keys sorted), `reason` the prune reason ("" when
+ * simulated). */
+typedef struct hp_log_entry {
+  uint64_t candidate;  /* byte offset of the descriptor in text */
+  uint64_t reason;     /* byte offset of the prune reason in text */
+  double time_s;       /* simulated iteration time; -1.0 when pruned */
+  int32_t task;        /* task index in build_tasks order: merge key across shards */
+  int32_t leaf;        /* leaf index inside the task (run_task order); -1 for task-level entries */
+} hp_log_entry;
+
+/* The log of the last hp_search on ctx made with HP_FLAG_LOG: this shard's
+ * entries in the reference's order. Sets *n_entries and *text_bytes; copies
+ * when entries/text are non-NULL and their capacities suffice (else
+ * HP_BAD_CONFIG). Shards own whole tasks (default mode) or whole leaves (full
+ * mode), so the global log is the stable merge of the shards' logs by
+ * (task, leaf). */
+hp_status hp_search_log(hp_ctx* ctx, hp_log_entry* entries, uint64_t entry_cap, char* text,
+                        uint64_t text_cap, uint64_t* n_entries, uint64_t* text_bytes);
 
 /* Argmin order of the reference (planner.cpp:178-200): returns <0 when
  * (time_a, plan_a) ranks before (time_b, plan_b), >0 after, 0 if identical.

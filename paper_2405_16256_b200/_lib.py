@@ -44,6 +44,9 @@ def lib():
     l.hp_better_than.restype = C.c_int
     l.hp_evaluate_plans.argtypes = [C.c_void_p, P(abi.hp_problem), P(abi.hp_plan), C.c_int32, P(C.c_double)]
     l.hp_evaluate_plans.restype = C.c_int
+    l.hp_search_log.argtypes = [C.c_void_p, P(abi.hp_log_entry), C.c_uint64, C.c_char_p, C.c_uint64,
+                                P(C.c_uint64), P(C.c_uint64)]
+    l.hp_search_log.restype = C.c_int
     if l.hp_abi_version() != abi_version():
         raise NativeLibraryMissing("libhetplan_b200.so ABI version mismatch; rebuild")
     _lib = l
@@ -55,4 +58,4 @@ def abi_version() -> int:
 
 
 EXPORTED = ["hp_abi_version", "hp_create", "hp_destroy", "hp_last_error", "hp_validate", "hp_probe",
-            "hp_search", "hp_better_than", "hp_evaluate_plans"]
+            "hp_search", "hp_search_log", "hp_better_than", "hp_evaluate_plans"]

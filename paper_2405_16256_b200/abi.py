@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-from typing import Dict, List, Tuple
+from typing import Dict, List, NamedTuple, Tuple
 
 HP_MAX_GROUPS = 8
 HP_MAX_STAGES = 256
@@ -23,6 +23,7 @@ HP_INTRA_NODE, HP_INTER_NODE, HP_INTER_GROUP = 0, 1, 2
 HP_GPU_DIRECT, HP_CPU_STAGED = 0, 1
 HP_REASON_COUNT = 4
 HP_FLAG_TIME_KERNELS = 1
+HP_FLAG_LOG = 2
 REASONS = ("memory", "bound", "no_link", "no_assignment")
 
 
@@ -91,6 +92,18 @@ class hp_result(C.Structure):
                 ("eval_launches", C.c_int64), ("eval_ms", C.c_double), ("eval_fp64_ops", C.c_double),
                 ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double), ("host_ms", C.c_double),
                 ("hill_iterations", C.c_int32), ("_pad1", C.c_int32), ("best_plan", hp_plan)]
+
+
+class hp_log_entry(C.Structure):
+    _fields_ = [("candidate", C.c_uint64), ("reason", C.c_uint64), ("time_s", C.c_double),
+                ("task", C.c_int32), ("leaf", C.c_int32)]
+
+
+class SearchLogEntry(NamedTuple):
+    """Reference SearchLogEntry (planner.hpp:95-99)."""
+    candidate: str       # compact JSON descriptor
+    time_s: float        # simulated time; -1.0 when pruned
+    prune_reason: str    # "" when simulated
 
 
 class ConfigError(ValueError):

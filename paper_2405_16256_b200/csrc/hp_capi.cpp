@@ -11,11 +11,13 @@
 #include "../../include/hetplan_b200.h"
 #include "hp_device.hpp"
 #include "hp_host.hpp"
+#include "hp_log.hpp"
 
 struct hp_ctx {
   hpd::Arena arena;
   std::string err;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  hpl::Log log;  // of the last hp_search with HP_FLAG_LOG
 };
 
 namespace {
@@ -139,16 +141,35 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   else mine = hph::shard_leaves(p, shard, nshard);
   result->host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
   ctx->arena.time_evals = opts && (opts->flags & HP_FLAG_TIME_KERNELS);
+  const bool want_log = opts && (opts->flags & HP_FLAG_LOG);
+  ctx->log.clear();
+  ctx->arena.log.reset();
+  ctx->arena.log.on = want_log;
   hpd::SearchOut out;
-  cudaEventRecord(ctx->ev0, ctx->arena.stream);
   hph::Status s;
-  if (p.pruning) {
-    bool have = opts && opts->have_global_bound;
-    s = hpd::search_default(ctx->arena, p, mine, have, have ? opts->global_bound : 0.0, false, out);
-  } else {
-    s = hpd::search_full(ctx->arena, p, mine, out);
+  for (int attempt = 0;; ++attempt) {
+    out = hpd::SearchOut{};
+    cudaEventRecord(ctx->ev0, ctx->arena.stream);
+    if (p.pruning) {
+      bool have = opts && opts->have_global_bound;
+      s = hpd::search_default(ctx->arena, p, mine, have, have ? opts->global_bound : 0.0, false, out);
+    } else {
+      s = hpd::search_full(ctx->arena, p, mine, out);
+    }
+    if (!s.ok()) {
+      ctx->arena.log.on = false;
+      return fail(ctx, s);
+    }
+    // a log that outgrew its buffers: the counters sized them, run again
+    if (!(want_log && ctx->arena.log.overflow) || attempt >= 2) break;
   }
-  if (!s.ok()) return fail(ctx, s);
+  ctx->arena.log.on = false;
+  if (want_log) {
+    if (ctx->arena.log.overflow) return fail(ctx, HP_INTERNAL, "search log: buffers overflowed twice");
+    s = hpl::build(p, ctx->arena.log, out.global_bound, shard == 0, ctx->log);
+    ctx->arena.log.reset();
+    if (!s.ok()) return fail(ctx, s);
+  }
   cudaEventRecord(ctx->ev1, ctx->arena.stream);
   cudaEventSynchronize(ctx->ev1);
   float ms = 0;
@@ -177,12 +198,35 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   } else {
     result->reason_counts[HP_REASON_MEMORY] += out.pruned;
   }
+  if (want_log && (ctx->log.simulated != result->candidates_simulated ||
+                   ctx->log.pruned != result->candidates_pruned)) {
+    ctx->log.clear();
+    return fail(ctx, HP_INTERNAL, "search log: replay counts differ from the GPU counts");
+  }
   if (out.has_best) {
     result->has_best = 1;
     result->best_time_s = out.best_time;
     const hph::LeafHost& lf = p.leaves[out.best_leaf];
     result->best_pp = p.tasks[lf.task].pp;
     hph::make_plan(p, lf, out.best_split.data(), result->best_plan);
+  }
+  return HP_OK;
+}
+
+hp_status hp_search_log(hp_ctx* ctx, hp_log_entry* entries, uint64_t entry_cap, char* text,
+                        uint64_t text_cap, uint64_t* n_entries, uint64_t* text_bytes) {
+  if (!ctx) return HP_INTERNAL;
+  if (!ctx->log.valid) return fail(ctx, HP_BAD_CONFIG, "no search log: run hp_search with HP_FLAG_LOG");
+  const uint64_t n = ctx->log.entries.size(), tb = ctx->log.text.size();
+  if (n_entries) *n_entries = n;
+  if (text_bytes) *text_bytes = tb;
+  if (entries) {
+    if (entry_cap < n) return fail(ctx, HP_BAD_CONFIG, "search log: entry buffer too small");
+    if (n) std::memcpy(entries, ctx->log.entries.data(), sizeof(hp_log_entry) * n);
+  }
+  if (text) {
+    if (text_cap < tb) return fail(ctx, HP_BAD_CONFIG, "search log: text buffer too small");
+    if (tb) std::memcpy(text, ctx->log.text.data(), tb);
   }
   return HP_OK;
 }

@@ -161,6 +161,8 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
     int* tbest = tbest_rows + td.best_off;
     TaskState ts{0.0, 0, -1, 0, 0, 0};
     const double gb = probe ? INF : global_bound;
+    int lseq = 0;  // search-log segment counter of this task (lane 0)
+    const bool logging = b.log.vals != nullptr && !probe;
 
     for (int li = td.leaf_begin; li < td.leaf_end; ++li) {
       const Leaf lf = b.leaves[li];
@@ -207,6 +209,10 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
           if (lane == 0) {
             ts.sim++;
             take_best(b, ts, tbest, li, split, t);
+            if (logging) {
+              const long long off = log_reserve(b.log, task, lseq++, 1);
+              if (off >= 0) b.log.vals[off] = t;
+            }
           }
         } else if (lane == 0) {
           if (act == 0) ts.pmem++;
@@ -274,6 +280,7 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
           if (lane == 0) {
             int comp[HP_MAX_STAGES];
             bool have_comp = false;
+            int nv = 0;  // simulated times, compacted into dec[0..nv) (nv <= k: not yet read)
             for (int k = 0; k < n; ++k) {
               unsigned char f = flag[k];
               if (f & 4) continue;  // memo hit
@@ -287,6 +294,7 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
                 continue;
               }
               double t = sc.times[xbase + (int)dec[k]];
+              dec[nv++] = t;
               ts.sim++;
               if (!ts.has_best || t <= ts.best_t) {
                 unrank_composition(base + k, c_consts.L, P, comp);
@@ -295,6 +303,11 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
               }
             }
             (void)have_comp;
+            if (logging) {
+              long long off = log_reserve(b.log, task, lseq++, nv);
+              if (off >= 0)
+                for (int j = 0; j < nv; ++j) b.log.vals[off + j] = dec[j];
+            }
           }
           ts.best_t = __shfl_sync(0xffffffffu, ts.best_t, 0);
           ts.has_best = __shfl_sync(0xffffffffu, ts.has_best, 0);
@@ -367,6 +380,7 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
           int nbs[HP_MAX_STAGES];
           int bq = -1;
           double bt = 0.0;
+          int nv = 0;
           // memo values of neighbours equal to the seeds
           for (int q = 0; q < nslots; ++q) {
             unsigned char f = flag[q];
@@ -388,6 +402,7 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
                 ts.pbound++;
               } else {
                 t = nbt[q];
+                dec[nv++] = t;
                 ts.sim++;
                 if (!ts.has_best || t <= ts.best_t) {
                   for (int i = 0; i < P; ++i) nbs[i] = cur[i];
@@ -401,6 +416,11 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
               bq = q;
               bt = t;
             }
+          }
+          if (logging) {
+            long long off = log_reserve(b.log, task, lseq++, nv);
+            if (off >= 0)
+              for (int j = 0; j < nv; ++j) b.log.vals[off + j] = dec[j];
           }
           if (bq >= 0 && bt < cur_t) {
             const int bb = bq >> 1, d = (bq & 1) ? -1 : 1;

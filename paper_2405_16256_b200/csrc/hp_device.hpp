@@ -11,6 +11,29 @@
 
 namespace hpd {
 
+// Raw search-log data of one search (HP_FLAG_LOG): the iteration times the
+// GPU simulated, per stream in the reference's visit order. hp_log.cpp
+// replays the reference's control flow over them to build the entries.
+struct LogRaw {
+  bool on = false;                      // requested for the next search
+  unsigned long long val_cap = 1ULL << 22, seg_cap = 1ULL << 20;
+  bool overflow = false;                // capacities grown; search must be re-run
+  // full mode: key = shard leaf position; default mode: key = device task position
+  std::vector<int> key_of;              // key -> global leaf (full) or global task (default)
+  std::vector<std::vector<double>> streams;
+  std::vector<double> tseed;            // full mode: uniform / proportional time per shard leaf
+  std::vector<double> exh;              // full mode: time per bounded rank, exhaustive leaves
+  std::vector<long long> exh_off;       // per shard leaf, -1 when not exhaustive
+  void reset() {
+    overflow = false;
+    key_of.clear();
+    streams.clear();
+    tseed.clear();
+    exh.clear();
+    exh_off.clear();
+  }
+};
+
 // Named, grow-only device buffers reused across searches on one context, so
 // repeated searches (benchmarks, sweeps) do not pay cudaMalloc each time.
 struct Arena {
@@ -40,6 +63,8 @@ struct Arena {
     }
     return markers[markers_used++ % markers.size()];
   }
+
+  LogRaw log;
 
   // optional per-launch timing of the evaluator kernels (bench roofline)
   bool time_evals = false;

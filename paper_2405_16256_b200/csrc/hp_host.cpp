@@ -383,6 +383,36 @@ void fill_consts(const Problem& p, hpc::Consts& c) {
   c.n_B = static_cast<int>(p.mbs.size());
 }
 
+hpc::Leaf device_leaf(const Problem& p, int li) {
+  const LeafHost& h = p.leaves[li];
+  const Task& t = p.tasks[h.task];
+  hpc::Leaf lf{};
+  lf.task = h.task;
+  lf.P = t.pp;
+  lf.M = static_cast<int>(h.M);
+  lf.dp = h.dp;
+  lf.B = h.B;
+  lf.B_idx = h.B_idx;
+  lf.layout_off = t.layout_off;
+  lf.mode = p.uniform_only ? 2 : (h.exhaustive ? 1 : 0);
+  lf.sched = p.schedule;
+  return lf;
+}
+
+void leaf_rows(const Problem& p, int li, hpc::LeafGroup* rows) {
+  const LeafHost& h = p.leaves[li];
+  for (int g = 0; g < static_cast<int>(p.groups.size()); ++g)
+    rows[g] = leaf_group(p, g, h.tp[g], h.B, h.dp, h.nodes[g]);
+}
+
+std::vector<double> hop_table(const Problem& p) {
+  std::vector<double> hop(p.mbs.size() * p.links.size());
+  for (size_t bi = 0; bi < p.mbs.size(); ++bi)
+    for (size_t l = 0; l < p.links.size(); ++l)
+      hop[bi * p.links.size() + l] = hop_time(p, static_cast<int>(l), p.mbs[bi]);
+  return hop;
+}
+
 // ------------------------------------------------------------ sharding
 
 std::vector<int> shard_leaves(const Problem& p, int shard, int count) {

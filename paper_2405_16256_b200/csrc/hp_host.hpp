@@ -89,6 +89,13 @@ std::vector<int> shard_tasks(const Problem& p, int shard, int count);
 std::string encode_plan(const Problem& p, const hp_plan& plan);
 int compare_plans(const Problem& p, double ta, const hp_plan& a, double tb, const hp_plan& b);
 
+// Device record and per-group cost rows of leaf `li` (split_off and lg_off
+// are left 0 for the caller to place). rows: n_groups entries.
+hpc::Leaf device_leaf(const Problem& p, int li);
+void leaf_rows(const Problem& p, int li, hpc::LeafGroup* rows);
+// hop_time per (micro-batch candidate, link): [n_B][n_links]
+std::vector<double> hop_table(const Problem& p);
+
 // make_plan (planner.cpp:553-575) for a leaf and split.
 void make_plan(const Problem& p, const LeafHost& lf, const int* split, hp_plan& out);
 

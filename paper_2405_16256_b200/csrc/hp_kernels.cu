@@ -63,6 +63,38 @@ __device__ __forceinline__ long long cand_id(const Work& w, int s) {
   return w.ids ? w.ids[w.first + s] : w.first + s;
 }
 
+// Search-log sink (HP_FLAG_LOG). Kernels append, per decided batch, the
+// iteration times of the candidates the reference simulates, in the
+// reference's visit order, as segments keyed (stream, seq); the host replays
+// the reference's control flow over them (hp_log.cpp). Capacity overflow is
+// detected from the counters, which keep counting past the capacity.
+struct LogSeg {
+  int key;             // shard leaf position (full mode) or shard task position (default)
+  int seq;             // hill step (full mode) or per-task batch counter (default)
+  long long off;       // first value in vals
+  long long n;
+};
+
+struct LogSink {
+  double* vals = nullptr;
+  LogSeg* segs = nullptr;
+  unsigned long long* ctr = nullptr;  // [0] values, [1] segments
+  unsigned long long val_cap = 0, seg_cap = 0;
+  double* exh = nullptr;              // full mode: time per bounded rank of exhaustive leaves
+  const long long* exh_off = nullptr;
+};
+
+// Reserves n values for segment (key, seq); returns their offset, or -1 when
+// n == 0 or the sink is full (the caller then writes nothing).
+__device__ inline long long log_reserve(const LogSink& s, int key, int seq, int n) {
+  if (n <= 0) return -1;
+  const unsigned long long off = atomicAdd(s.ctr, (unsigned long long)n);
+  const unsigned long long k = atomicAdd(s.ctr + 1, 1ULL);
+  if (off + n > s.val_cap || k >= s.seg_cap) return -1;
+  s.segs[k] = LogSeg{key, seq, (long long)off, (long long)n};
+  return (long long)off;
+}
+
 struct Bufs {
   const Leaf* leaves;
   const LeafGroup* lg;
@@ -86,6 +118,7 @@ struct Bufs {
   const long long* etbl;
   const int* etbl_off;
   const int* ecap;
+  LogSink log;
 };
 
 // count of bounded compositions continuing with part value v at position j
@@ -673,10 +706,21 @@ __global__ void __launch_bounds__(256) k_hill_async(Bufs b, AsyncQ q, int cls) {
         unsigned char old[2 * HP_MAX_STAGES];
         int tmp[HP_MAX_STAGES];
         for (int i = 0; i < lf.P; ++i) delta[i] = 0;
+        const int seq = hs.steps;
         hill_step(c_consts, lf, b.lg + lf.lg_off, b.layouts + lf.layout_off, b.cur + lf.split_off,
                   b.uni + lf.split_off, b.prop + lf.split_off, b.best + lf.split_off,
                   b.hist + b.hist_off[li], hs, b.nb + b.nb_off[li], delta, old, tmp);
         b.hs[li] = hs;
+        if (b.log.vals) {  // simulated, non-memo neighbours in visit order (planner.cpp:472-476)
+          const double* nbt = b.nb + b.nb_off[li];
+          const int nslots = 2 * (lf.P - 1);
+          int n = 0;
+          for (int q = 0; q < nslots; ++q) n += (!old[q] && nbt[q] >= 0) ? 1 : 0;
+          long long off = log_reserve(b.log, li, seq, n);
+          if (off >= 0)
+            for (int q = 0; q < nslots; ++q)
+              if (!old[q] && nbt[q] >= 0) b.log.vals[off++] = nbt[q];
+        }
         if (b.trace) {
           unsigned long long now;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
@@ -740,6 +784,7 @@ __global__ void k_exh_reduce(Bufs b, const ExhSpan* spans, int n_spans) {
   int comp[HP_MAX_STAGES];
   for (long long j = 0; j < sp.n; ++j) {
     double t = b.xbuf[sp.out + j];
+    if (b.log.exh) b.log.exh[b.log.exh_off[sp.leaf] + sp.first + j] = t;
     if (t < 0) {
       hs.pruned++;
       continue;
@@ -976,6 +1021,7 @@ __global__ void __launch_bounds__(128) k_exh_thread(Bufs b, const ExhItem* items
       dps[i] = dp_sync(row, comp[i]);
     }
     const double t = sim_thread<P>(lf.M, f, bw, sf, sb, dps);
+    if (b.log.exh) b.log.exh[b.log.exh_off[w.leaf] + r0 + k] = t;
     ++sim;
     if (brank < 0 || t < bt || (t == bt && enc_less_t<P>(comp, bcomp))) {
       bt = t;
@@ -1251,36 +1297,22 @@ static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vect
   leaves.assign(nL, Leaf{});
   std::vector<LeafGroup> lgs((size_t)nL * G);
   std::vector<int> hist_off(nL), nb_off(nL);
-  std::vector<double> hop(p.mbs.size() * p.links.size());
-  for (size_t bi = 0; bi < p.mbs.size(); ++bi)
-    for (size_t l = 0; l < p.links.size(); ++l)
-      hop[bi * p.links.size() + l] = hph::hop_time(p, (int)l, p.mbs[bi]);
+  std::vector<double> hop = hph::hop_table(p);
   int split_total = 0, hist_total = 0, nb_total = 0;
   hill_ids.clear();
   exh_ids.clear();
   for (int k = 0; k < nL; ++k) {
-    const hph::LeafHost& h = p.leaves[my_leaves[k]];
-    const hph::Task& t = p.tasks[h.task];
     Leaf& lf = leaves[k];
-    lf.task = h.task;
-    lf.P = t.pp;
-    lf.M = static_cast<int>(h.M);
-    lf.dp = h.dp;
-    lf.B = h.B;
-    lf.B_idx = h.B_idx;
-    lf.layout_off = t.layout_off;
+    lf = hph::device_leaf(p, my_leaves[k]);
     lf.split_off = split_total;
     lf.lg_off = k * G;
-    lf.mode = p.uniform_only ? 2 : (h.exhaustive ? 1 : 0);
-    lf.sched = p.schedule;
-    split_total += t.pp;
-    for (int g = 0; g < G; ++g)
-      lgs[(size_t)k * G + g] = hph::leaf_group(p, g, h.tp[g], h.B, h.dp, h.nodes[g]);
+    split_total += lf.P;
+    hph::leaf_rows(p, my_leaves[k], &lgs[(size_t)k * G]);
     hist_off[k] = hist_total;
     nb_off[k] = nb_total;
     if (lf.mode == 0) {
       hist_total += 4 * p.model.num_layers;
-      nb_total += 2 * (t.pp - 1);
+      nb_total += 2 * (lf.P - 1);
     }
     if (lf.mode == 1) exh_ids.push_back(k);
     else hill_ids.push_back(k);
@@ -1317,6 +1349,49 @@ static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vect
   return hph::Status{};
 }
 
+// Search-log sink buffers at the arena's current capacities.
+static hph::Status log_open(Arena& a, hpk::LogSink& sink) {
+  hph::Status s;
+  sink = hpk::LogSink{};
+  if (!(s = scratch(a, "log_ctr", 2, &sink.ctr)).ok()) return s;
+  if (!(s = scratch(a, "log_vals", a.log.val_cap, &sink.vals)).ok()) return s;
+  if (!(s = scratch(a, "log_segs", a.log.seg_cap, &sink.segs)).ok()) return s;
+  sink.val_cap = a.log.val_cap;
+  sink.seg_cap = a.log.seg_cap;
+  CK(cudaMemsetAsync(sink.ctr, 0, 2 * sizeof(unsigned long long), a.stream));
+  return s;
+}
+
+// Reads the segments back and orders them into per-key streams. On overflow
+// grows the capacities and flags the search for a re-run.
+static hph::Status log_collect(Arena& a, const hpk::LogSink& sink, size_t n_keys) {
+  unsigned long long ctr[2];
+  CK(cudaMemcpyAsync(ctr, sink.ctr, sizeof ctr, cudaMemcpyDeviceToHost, a.stream));
+  CK(cudaStreamSynchronize(a.stream));
+  if (ctr[0] > a.log.val_cap || ctr[1] > a.log.seg_cap) {
+    a.log.overflow = true;
+    a.log.val_cap = std::max(a.log.val_cap, ctr[0] + ctr[0] / 8 + 1024);
+    a.log.seg_cap = std::max(a.log.seg_cap, ctr[1] + ctr[1] / 8 + 1024);
+    return hph::Status{};
+  }
+  std::vector<hpk::LogSeg> segs(ctr[1]);
+  std::vector<double> vals(ctr[0]);
+  if (ctr[1]) CK(cudaMemcpy(segs.data(), sink.segs, sizeof(hpk::LogSeg) * ctr[1], cudaMemcpyDeviceToHost));
+  if (ctr[0]) CK(cudaMemcpy(vals.data(), sink.vals, sizeof(double) * ctr[0], cudaMemcpyDeviceToHost));
+  a.d2h_bytes += sizeof ctr + sizeof(hpk::LogSeg) * ctr[1] + sizeof(double) * ctr[0];
+  std::sort(segs.begin(), segs.end(), [](const hpk::LogSeg& x, const hpk::LogSeg& y) {
+    return x.key != y.key ? x.key < y.key : x.seq < y.seq;
+  });
+  a.log.streams.assign(n_keys, {});
+  for (const hpk::LogSeg& g : segs) {
+    if (g.key < 0 || static_cast<size_t>(g.key) >= n_keys)
+      return hph::Status{HP_INTERNAL, "search log: bad segment key"};
+    auto& v = a.log.streams[g.key];
+    v.insert(v.end(), vals.begin() + g.off, vals.begin() + g.off + g.n);
+  }
+  return hph::Status{};
+}
+
 hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>& my_leaves,
                         SearchOut& out) {
   cudaStream_t st = a.stream;
@@ -1326,6 +1401,11 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   std::vector<int> hill_ids, exh_ids;
   hph::Status s = setup_tables(a, p, my_leaves, b, leaves, hill_ids, exh_ids);
   if (!s.ok()) return s;
+  if (a.log.on) {
+    a.log.reset();
+    a.log.key_of = my_leaves;
+    if (!(s = log_open(a, b.log)).ok()) return s;
+  }
 
   // counters: [0..7] items per class, [8..15] next-item per class,
   // [16] n_active, [17] n_next, [18..19] one-off queue count / next
@@ -1546,6 +1626,19 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     CK(cudaMemcpyAsync(feas.data(), d_feas, sizeof(long long) * nL, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     a.d2h_bytes += sizeof(long long) * nL;
+    if (a.log.on) {  // per-rank times of the exhaustive leaves for the log
+      a.log.exh_off.assign(nL, -1);
+      long long tot = 0;
+      for (int k : exh_ids) {
+        a.log.exh_off[k] = tot;
+        tot += feas[k];
+      }
+      long long* d_xo;
+      if (!(s = upload(a, "log_exh_off", a.log.exh_off, &d_xo)).ok()) return s;
+      if (!(s = scratch(a, "log_exh", (size_t)tot, &b.log.exh)).ok()) return s;
+      b.log.exh_off = d_xo;
+      a.log.exh.resize(tot);
+    }
 
     // thread path: 1F1B with M >= P and P <= 8
     std::vector<std::vector<hpk::ExhItem>> titems(9);
@@ -1656,6 +1749,15 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     }
     hpk::k_exh_fix<<<(ne + T - 1) / T, T, 0, st>>>(b, d_exh_ids, ne, d_feas);
     out.launches++;
+  }
+
+  if (a.log.on) {
+    if (!(s = log_collect(a, b.log, my_leaves.size())).ok()) return s;
+    a.log.tseed.resize(2 * (size_t)nL);
+    if (nL) CK(cudaMemcpy(a.log.tseed.data(), b.tseed, sizeof(double) * 2 * nL, cudaMemcpyDeviceToHost));
+    if (!a.log.exh.empty())
+      CK(cudaMemcpy(a.log.exh.data(), b.log.exh, sizeof(double) * a.log.exh.size(), cudaMemcpyDeviceToHost));
+    a.d2h_bytes += sizeof(double) * (2.0 * nL + a.log.exh.size());
   }
 
   // ---- final argmin
@@ -1875,6 +1977,7 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   cudaStream_t st = a.stream;
   std::vector<int> my_leaves;
   std::vector<hpk::TaskDev> tasks;
+  std::vector<int> task_ids;  // device task position -> global task
   int best_total = 0;
   for (int ti : my_tasks) {
     const hph::Task& t = p.tasks[ti];
@@ -1885,7 +1988,10 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
     td.pp = t.pp;
     td.best_off = best_total;
     best_total += t.pp;
-    if (td.leaf_end > td.leaf_begin) tasks.push_back(td);
+    if (td.leaf_end > td.leaf_begin) {
+      tasks.push_back(td);
+      task_ids.push_back(ti);
+    }
   }
   hpk::Bufs b;
   std::vector<Leaf> leaves;
@@ -1935,6 +2041,11 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
     if (probe_only) return hph::Status{};
   }
   CK(cudaMemsetAsync(d_next, 0, sizeof(int), st));
+  if (a.log.on) {
+    a.log.reset();
+    a.log.key_of = task_ids;
+    if (!(s = log_open(a, b.log)).ok()) return s;
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (a.time_evals) {
     a.event_pair(&e0, &e1);
@@ -1960,6 +2071,7 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   CK(cudaMemcpyAsync(&ops, d_ops, sizeof ops, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (a.time_evals) out.eval_ms = a.drain_events();
+  if (a.log.on && !(s = log_collect(a, b.log, tasks.size())).ok()) return s;
   out.eval_fp64_ops = static_cast<double>(ops);
   out.simulated = counts[0];
   out.pruned = counts[1] + counts[2];

@@ -1,6 +1,6 @@
 """Host-side mirror of the reference planner interface for the hot path.
 
-    search(docs, jobs=1) -> SearchOutcome          (planner.hpp:115-116)
+    search(docs, jobs=1, log=False) -> SearchOutcome   (planner.hpp:115-116)
     evaluate_plans(docs, plans) -> [iteration_time_s]  (evaluate.hpp:56-58, batched)
 
 `docs` are the reference's own JSON documents {"model","cluster","train",
@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 from dataclasses import dataclass, field
-from typing import Dict, List, Optional
+from typing import Dict, List, Optional, Tuple
 
 from . import abi
 from ._lib import lib
@@ -34,6 +34,7 @@ class SearchOutcome:
     tasks: int = 0
     global_bound: float = math.inf
     raw: Optional[abi.hp_result] = None
+    log: List[abi.SearchLogEntry] = field(default_factory=list)  # SearchOutcome::log (when requested)
 
 
 class Engine:
@@ -67,14 +68,38 @@ class Engine:
         raise RuntimeError(f"{what} failed (status {st}): {msg}")
 
     def search_shard(self, problem: abi.Problem, shard_index: int = 0, shard_count: int = 1,
-                     global_bound: Optional[float] = None) -> abi.hp_result:
-        opts = abi.hp_search_opts(shard_index, shard_count, int(global_bound is not None), 0,
+                     global_bound: Optional[float] = None, flags: int = 0) -> abi.hp_result:
+        opts = abi.hp_search_opts(shard_index, shard_count, int(global_bound is not None), flags,
                                   global_bound if global_bound is not None else 0.0)
         res = abi.hp_result()
         st = self._lib.hp_search(self._ctx, problem.ptr(), C.byref(opts), C.byref(res))
         if st != abi.HP_OK:
             self._raise(st, "hp_search")
         return res
+
+    def search_log(self) -> List[Tuple[int, int, abi.SearchLogEntry]]:
+        """The log of the last search_shard(flags=HP_FLAG_LOG): (task, leaf,
+        entry) in the reference's order for this shard."""
+        n = C.c_uint64()
+        nb = C.c_uint64()
+        st = self._lib.hp_search_log(self._ctx, None, 0, None, 0, C.byref(n), C.byref(nb))
+        if st != abi.HP_OK:
+            self._raise(st, "hp_search_log")
+        ents = (abi.hp_log_entry * max(1, n.value))()
+        text = C.create_string_buffer(max(1, nb.value))
+        st = self._lib.hp_search_log(self._ctx, ents, n.value, text, nb.value, C.byref(n), C.byref(nb))
+        if st != abi.HP_OK:
+            self._raise(st, "hp_search_log")
+        raw = text.raw
+        out = []
+        for k in range(n.value):
+            e = ents[k]
+            c0 = e.candidate
+            r0 = e.reason
+            cand = raw[c0:raw.index(b"\0", c0)].decode()
+            reason = raw[r0:raw.index(b"\0", r0)].decode()
+            out.append((e.task, e.leaf, abi.SearchLogEntry(cand, e.time_s, reason)))
+        return out
 
     def probe_shard(self, problem: abi.Problem, shard_index: int = 0, shard_count: int = 1) -> float:
         opts = abi.hp_search_opts(shard_index, shard_count, 0, 0, 0.0)
@@ -112,14 +137,49 @@ def _outcome(problem: abi.Problem, res: abi.hp_result) -> SearchOutcome:
                          tasks=res.tasks, global_bound=res.global_bound, raw=res)
 
 
-def search(docs: Dict[str, dict], jobs: int = 1, device: int = 0) -> SearchOutcome:
+def infeasible_reasons(log: List[abi.SearchLogEntry], n_tasks: int) -> List[str]:
+    """InfeasibleError reasons of planner.cpp:666-678: the first 200 distinct
+    "candidate -> reason" lines of the log."""
+    reasons, seen = [], set()
+    for e in log:
+        if not e.prune_reason:
+            continue
+        line = e.candidate + " -> " + e.prune_reason
+        if line not in seen:
+            seen.add(line)
+            if len(reasons) < 200:
+                reasons.append(line)
+    if n_tasks == 0:
+        reasons.append("no usable pipeline degree: candidates must lie in [1, num_layers] and fit the "
+                       "cluster's node counts")
+    return reasons
+
+
+def merge_logs(parts: List[List[Tuple[int, int, abi.SearchLogEntry]]]) -> List[abi.SearchLogEntry]:
+    """Global log from per-shard logs: shards own whole tasks or whole leaves,
+    so a stable sort on (task, leaf) restores the reference's order."""
+    allp = [x for part in parts for x in part]
+    allp.sort(key=lambda x: (x[0], x[1]))
+    return [x[2] for x in allp]
+
+
+def search(docs: Dict[str, dict], jobs: int = 1, device: int = 0, log: bool = False) -> SearchOutcome:
     """search() of planner.hpp:115-116 on one GPU (`jobs` is accepted for
-    signature parity; the GPU replaces the thread pool)."""
+    signature parity; the GPU replaces the thread pool). log=True fills
+    SearchOutcome.log; an infeasible search raises InfeasibleError with the
+    reference's reason list (taken from the log)."""
     problem = abi.Problem(docs)
-    res = engine(device).search_shard(problem)
+    eng = engine(device)
+    res = eng.search_shard(problem, flags=abi.HP_FLAG_LOG if log else 0)
+    entries = merge_logs([eng.search_log()]) if log else []
     if not res.has_best:
-        raise abi.InfeasibleError("no feasible plan found")
-    return _outcome(problem, res)
+        if not log:
+            eng.search_shard(problem, flags=abi.HP_FLAG_LOG)
+            entries = merge_logs([eng.search_log()])
+        raise abi.InfeasibleError("no feasible plan found", infeasible_reasons(entries, res.tasks))
+    out = _outcome(problem, res)
+    out.log = entries
+    return out
 
 
 def evaluate_plans(docs: Dict[str, dict], plans: List[dict], device: int = 0) -> List[float]:
@@ -172,7 +232,7 @@ def gather_results(res: abi.hp_result, world: int, group=None, device=None) -> L
 
 
 def search_sharded(docs: Dict[str, dict], rank: int, world: int, device: Optional[int] = None, group=None,
-                   shard_fn=None, probe_fn=None) -> SearchOutcome:
+                   shard_fn=None, probe_fn=None, log: bool = False) -> SearchOutcome:
     """One shard per rank; default mode first all-reduces (MIN) the per-shard
     probe bounds (planner.cpp:640-651), then every rank searches its shard and
     the per-rank records are all-gathered in one collective; every rank
@@ -183,10 +243,13 @@ def search_sharded(docs: Dict[str, dict], rank: int, world: int, device: Optiona
     import torch.distributed as dist
 
     problem = abi.Problem(docs)
+    log_fn = None
     if shard_fn is None:
         eng = engine(device)
-        shard_fn = lambda p, r, w, b: eng.search_shard(p, r, w, b)  # noqa: E731
+        flags = abi.HP_FLAG_LOG if log else 0
+        shard_fn = lambda p, r, w, b: eng.search_shard(p, r, w, b, flags)  # noqa: E731
         probe_fn = lambda p, r, w: eng.probe_shard(p, r, w)  # noqa: E731
+        log_fn = eng.search_log
     bound = None
     if problem.struct.planner.time_bound_pruning:
         b = probe_fn(problem, rank, world)
@@ -195,6 +258,13 @@ def search_sharded(docs: Dict[str, dict], rank: int, world: int, device: Optiona
         bound = float(t.item())
     res = shard_fn(problem, rank, world, bound)
     red = reduce_results(problem, gather_results(res, world, group, device))
+    entries = []
+    if log and log_fn is not None:
+        parts = [None] * world
+        dist.all_gather_object(parts, log_fn(), group=group)  # cold path: variable-size log
+        entries = merge_logs(parts)
     if not red.has_best:
-        raise abi.InfeasibleError("no feasible plan found")
-    return _outcome(problem, red)
+        raise abi.InfeasibleError("no feasible plan found", infeasible_reasons(entries, red.tasks))
+    out = _outcome(problem, red)
+    out.log = entries
+    return out

@@ -1,0 +1,89 @@
+"""Search-log parity (SearchOutcome::log, planner.hpp:95-107; SURVEY §8f
+row 1) through the C ABI: every golden case's log (entry count, SHA-256 of
+all entries, first entries verbatim) against the compiled reference's
+(tests/golden/search_logs.json), the InfeasibleError reason list
+(planner.cpp:666-678), and shard-merged logs equal to the single-device log.
+"""
+from __future__ import annotations
+
+import hashlib
+import struct
+
+import pytest
+
+from conftest import load_golden
+from paper_2405_16256_b200 import abi, planner
+
+pytestmark = pytest.mark.gpu
+
+
+def time_bits(t: float) -> str:
+    return "%016x" % struct.unpack("<Q", struct.pack("<d", t))[0]
+
+
+def rows(entries):
+    return [(e.candidate, time_bits(e.time_s), e.prune_reason) for e in entries]
+
+
+def digest(rs) -> str:
+    h = hashlib.sha256()
+    for c, b, r in rs:
+        h.update(f"{c}\t{b}\t{r}\n".encode())
+    return h.hexdigest()
+
+
+@pytest.fixture(scope="module")
+def logs():
+    return {c["name"]: c for c in load_golden("search_logs.json")}
+
+
+def test_logs_match_reference(engine, search_cases, logs):
+    checked = 0
+    for case in search_cases:
+        want = logs[case["name"]]
+        if want["status"] != 0:
+            continue
+        out = planner.search(case["docs"], log=True)
+        got = rows(out.log)
+        assert got[:len(want["head"])] == [tuple(x) for x in want["head"]], case["name"]
+        assert len(got) == want["n"], case["name"]
+        assert digest(got) == want["sha256"], case["name"]
+        assert len(got) == out.candidates_simulated + out.candidates_pruned
+        checked += 1
+    assert checked > 100
+
+
+def test_infeasible_reasons_match_reference(engine, search_cases, logs):
+    n = 0
+    for case in search_cases:
+        want = logs[case["name"]]
+        if want["status"] != 2:
+            continue
+        with pytest.raises(abi.InfeasibleError) as ei:
+            planner.search(case["docs"])
+        assert ei.value.reasons == want["reasons"], case["name"]
+        n += 1
+    assert n > 0
+
+
+@pytest.mark.parametrize("shards", [2, 3])
+def test_sharded_logs_merge_to_reference(engine, search_cases, logs, shards):
+    picked = [c for c in search_cases if logs[c["name"]]["status"] == 0][:40]
+    for case in picked:
+        p = abi.Problem(case["docs"])
+        bound = None
+        if p.struct.planner.time_bound_pruning:
+            bound = min(engine.probe_shard(p, k, shards) for k in range(shards))
+        parts = []
+        for k in range(shards):
+            engine.search_shard(p, k, shards, bound, abi.HP_FLAG_LOG)
+            parts.append(engine.search_log())
+        got = rows(planner.merge_logs(parts))
+        assert digest(got) == logs[case["name"]]["sha256"], (case["name"], shards)
+
+
+def test_log_needs_flag(engine, search_cases):
+    p = abi.Problem(search_cases[0]["docs"])
+    engine.search_shard(p)
+    with pytest.raises(abi.ConfigError):
+        engine.search_log()
