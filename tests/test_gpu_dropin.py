@@ -1,0 +1,127 @@
+"""The drop-in boundary end to end: the reference's own code
+with hetplan::search (planner.hpp:115-116) replaced by
+integration/hetplan_search_b200.cpp, running on the GPU.
+
+* integration/_build/libhetplan_dropin.so — the unmodified reference library
+  plus the B200 search, driven through the same JSON driver as oracle/_ref:
+  plans, iteration-time bits, candidate counts and search logs equal the
+  golden fixtures of the reference.
+* integration/_build/hetplan_plan_b200 — the reference CLI's `plan` command
+  (tools/cli.cpp:216-260) over the B200 search: plan.json, report.json,
+  search_log.ndjson, stdout and exit codes byte-identical to the same front
+  end over the reference CPU search (oracle/_ref/hetplan_plan_ref).
+"""
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import json
+import os
+import random
+import subprocess
+
+import pytest
+
+from conftest import ROOT, load_golden
+from instances import random_instance
+from paper_2405_16256_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+DROPIN = os.path.join(ROOT, "integration", "_build", "libhetplan_dropin.so")
+PLAN_B200 = os.path.join(ROOT, "integration", "_build", "hetplan_plan_b200")
+PLAN_REF = os.path.join(ROOT, "oracle", "_ref", "hetplan_plan_ref")
+
+
+def _need(path):
+    if not os.path.exists(path):
+        pytest.fail(f"{path} missing: build with `make -C integration` / `make -C oracle ref`")
+
+
+@pytest.fixture(scope="module")
+def dropin():
+    _need(DROPIN)
+    l = ctypes.CDLL(DROPIN)
+    cp = ctypes.c_char_p
+    l.ref_search_json.argtypes = [cp, cp, cp, cp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+    l.ref_search_json.restype = ctypes.c_int
+    l.ref_free.argtypes = [ctypes.c_void_p]
+
+    def search(docs, want_log=False):
+        out = ctypes.c_void_p()
+        enc = [json.dumps(docs[k]).encode() for k in ("model", "cluster", "train", "planner")]
+        l.ref_search_json(*enc, 1, int(want_log), ctypes.byref(out))
+        s = ctypes.string_at(out.value).decode()
+        l.ref_free(out)
+        return json.loads(s)
+
+    return search
+
+
+def _digest(log):
+    h = hashlib.sha256()
+    for e in log:
+        h.update(f"{e['candidate']}\t{e['time_bits']}\t{e['reason']}\n".encode())
+    return h.hexdigest()
+
+
+def test_dropin_library_matches_reference(dropin, search_cases):
+    logs = {c["name"]: c for c in load_golden("search_logs.json")}
+    for case in search_cases:
+        r = dropin(case["docs"], want_log=True)
+        assert r["status"] == case["status"], case["name"]
+        if case["status"] != 0:
+            assert r.get("reasons", []) == logs[case["name"]]["reasons"], case["name"]
+            continue
+        assert r["eval"]["iteration_bits"] == case["iteration_bits"], case["name"]
+        assert r["plan"] == case["plan"], case["name"]
+        assert (r["candidates_simulated"], r["candidates_pruned"]) == (
+            case["candidates_simulated"], case["candidates_pruned"]), case["name"]
+        assert len(r["log"]) == logs[case["name"]]["n"], case["name"]
+        assert _digest(r["log"]) == logs[case["name"]]["sha256"], case["name"]
+
+
+def _write_inputs(d, docs):
+    paths = {}
+    for k in ("model", "cluster", "train", "planner"):
+        p = os.path.join(d, f"{k}.json")
+        with open(p, "w") as f:
+            json.dump(docs[k], f, indent=2)
+        paths[k] = p
+    return paths
+
+
+def _run_plan(binary, paths, out):
+    cmd = [binary, "--model", paths["model"], "--cluster", paths["cluster"], "--train", paths["train"],
+           "--planner", paths["planner"], "--out", out, "--jobs", "4"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    files = {}
+    for name in ("plan.json", "report.json", "search_log.ndjson"):
+        fp = os.path.join(out, name)
+        if os.path.exists(fp):
+            files[name] = open(fp, "rb").read()
+    return r.returncode, r.stdout.replace(out, "<OUT>"), r.stderr, files
+
+
+def _cli_cases():
+    cases = [("C0-full", configs.config("C0", full=True)), ("C0-default", configs.config("C0", full=False)),
+             ("C1-default", configs.config("C1", full=False)), ("C2u-full", configs.config("C2u", full=True))]
+    rng = random.Random(7)
+    for k in range(12):
+        cases.append((f"rand{k}", random_instance(rng, k)))
+    return cases
+
+
+@pytest.mark.parametrize("name,docs", _cli_cases(), ids=lambda x: x if isinstance(x, str) else "")
+def test_cli_plan_outputs_byte_identical(tmp_path, name, docs):
+    _need(PLAN_B200)
+    _need(PLAN_REF)
+    paths = _write_inputs(str(tmp_path), docs)
+    got = _run_plan(PLAN_B200, paths, str(tmp_path / "b200"))
+    want = _run_plan(PLAN_REF, paths, str(tmp_path / "ref"))
+    assert got[0] == want[0], (name, got[2], want[2])
+    assert got[1].replace("/b200", "/X") == want[1].replace("/ref", "/X"), name
+    assert got[2] == want[2], name
+    assert sorted(got[3]) == sorted(want[3]), name
+    for k in want[3]:
+        assert got[3][k] == want[3][k], (name, k)

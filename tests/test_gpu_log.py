@@ -87,3 +87,28 @@ def test_log_needs_flag(engine, search_cases):
     engine.search_shard(p)
     with pytest.raises(abi.ConfigError):
         engine.search_log()
+
+
+def test_c3_default_log_matches_reference(engine):
+    from paper_2405_16256_b200 import configs
+    want = load_golden("c3_default_log.json")
+    out = planner.search(configs.config("C3", full=False), log=True)
+    got = rows(out.log)
+    assert got[:4] == [tuple(x) for x in want["head"]]
+    assert len(got) == want["n"]
+    assert digest(got) == want["sha256"]
+
+
+def test_c3_full_log_is_complete(engine):
+    """C3 full sweep with the log (10.5 M entries; the reference needs ~8 CPU-
+    hours for it, so no digest): the replay consumes every GPU time and its
+    counts equal the GPU's (checked inside hp_search), one entry per
+    candidate."""
+    import ctypes as C
+    from paper_2405_16256_b200 import configs
+    p = abi.Problem(configs.config("C3", full=True))
+    res = engine.search_shard(p, flags=abi.HP_FLAG_LOG)
+    n = C.c_uint64()
+    nb = C.c_uint64()
+    assert engine._lib.hp_search_log(engine._ctx, None, 0, None, 0, C.byref(n), C.byref(nb)) == abi.HP_OK
+    assert n.value == res.candidates_simulated + res.candidates_pruned == 10513178
