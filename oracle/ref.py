@@ -39,6 +39,8 @@ def lib():
         l.ref_split_layers.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
                                        ctypes.POINTER(ctypes.c_int)]
         l.ref_split_layers.restype = ctypes.c_int
+        l.ref_calibrate_json.argtypes = [cp, cp, cp, ctypes.POINTER(ctypes.c_void_p)]
+        l.ref_calibrate_json.restype = ctypes.c_int
         l.ref_free.argtypes = [ctypes.c_void_p]
         _lib = l
     return _lib
@@ -65,6 +67,13 @@ def evaluate(cfg: dict, plan: dict) -> dict:
     out = ctypes.c_void_p()
     enc = [json.dumps(cfg[k]).encode() for k in ("model", "cluster", "train")] + [json.dumps(plan).encode()]
     lib().ref_evaluate_json(*enc, ctypes.byref(out))
+    return _take(out)
+
+
+def calibrate(model: dict, cluster: dict, profiles_text: str) -> dict:
+    out = ctypes.c_void_p()
+    lib().ref_calibrate_json(json.dumps(model).encode(), json.dumps(cluster).encode(),
+                             profiles_text.encode(), ctypes.byref(out))
     return _take(out)
 
 

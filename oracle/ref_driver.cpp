@@ -22,6 +22,7 @@
 #include "hetplan/evaluate.hpp"
 #include "hetplan/json_io.hpp"
 #include "hetplan/planner.hpp"
+#include "hetplan/profile.hpp"
 
 using nlohmann::json;
 
@@ -150,6 +151,40 @@ int ref_simulate(int schedule_gpipe, const double* times, int P, long long M,
   } catch (const std::exception&) {
     return 3;
   }
+}
+
+// parse_profiles + calibrate (profile.cpp:63-135), as cli.cpp:107-114 runs
+// them: the calibrated cluster, its per-group scalars as bit patterns, and
+// the diagnostics in CLI order (parse first, then calibration).
+int ref_calibrate_json(const char* model, const char* cluster, const char* profiles, char** out) {
+  json result;
+  int status = 0;
+  try {
+    hetplan::ModelSpec m = hetplan::model_from_json(json::parse(model));
+    hetplan::ClusterSpec c = hetplan::cluster_from_json(json::parse(cluster));
+    hetplan::ParsedProfiles parsed = hetplan::parse_profiles(std::string(profiles));
+    hetplan::CalibrationResult cal = hetplan::calibrate(parsed.records, m, c);
+    json diags = json::array();
+    for (const auto& d : parsed.diagnostics) diags.push_back("profiles: " + d);
+    for (const auto& d : cal.diagnostics) diags.push_back("calibration: " + d);
+    json groups = json::array();
+    for (const auto& g : cal.cluster.groups)
+      groups.push_back(json{{"name", g.name},
+                            {"compute_efficiency_bits", hex_bits(g.compute_efficiency)},
+                            {"bwd_fwd_ratio_bits", hex_bits(g.bwd_fwd_ratio)}});
+    result["cluster"] = hetplan::to_json(cal.cluster);
+    result["groups"] = groups;
+    result["diagnostics"] = diags;
+  } catch (const hetplan::ConfigError& e) {
+    status = 1;
+    result["error"] = e.what();
+  } catch (const std::exception& e) {
+    status = 3;
+    result["error"] = e.what();
+  }
+  result["status"] = status;
+  *out = dup_string(result.dump());
+  return status;
 }
 
 // split_layers (planner.cpp:42-84). Returns 0, 1 ConfigError, 2 InfeasibleError.

@@ -94,6 +94,8 @@ def _write_inputs(d, docs):
 def _run_plan(binary, paths, out):
     cmd = [binary, "--model", paths["model"], "--cluster", paths["cluster"], "--train", paths["train"],
            "--planner", paths["planner"], "--out", out, "--jobs", "4"]
+    if "profiles" in paths:
+        cmd += ["--profiles", paths["profiles"]]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     files = {}
     for name in ("plan.json", "report.json", "search_log.ndjson"):
@@ -125,3 +127,45 @@ def test_cli_plan_outputs_byte_identical(tmp_path, name, docs):
     assert sorted(got[3]) == sorted(want[3]), name
     for k in want[3]:
         assert got[3][k] == want[3][k], (name, k)
+
+
+def _profiles(rng, groups):
+    lines = []
+    for g in groups:
+        for _ in range(rng.randrange(1, 4)):
+            lines.append(json.dumps({"device_type": g, "micro_batch": rng.choice([1, 2]), "seq_length": 4096,
+                                     "hidden": 8192, "tp_degree": rng.choice([4, 8]),
+                                     "fwd_ms": round(rng.uniform(5.0, 30.0), 3),
+                                     "bwd_ms": round(rng.uniform(10.0, 70.0), 3)}))
+    lines.append(json.dumps({"device_type": "ghost", "micro_batch": 1, "seq_length": 1, "hidden": 1,
+                             "fwd_ms": 1.0, "bwd_ms": 2.0}))
+    return "\n".join(lines) + "\n"
+
+
+@pytest.mark.parametrize("cfg", ["C0", "C1", "C2u"])
+def test_cli_plan_with_profiles(tmp_path, cfg):
+    """`plan --profiles` (calibration, cli.cpp:107-114, then search): the
+    drop-in CLI equals the reference CLI byte for byte, and the Python path
+    (calibrate.calibrate_docs + planner.search) finds the same plan."""
+    from paper_2405_16256_b200 import abi, calibrate, planner
+    _need(PLAN_B200)
+    _need(PLAN_REF)
+    docs = configs.config(cfg, full=False)
+    rng = random.Random(sum(map(ord, cfg)))
+    text = _profiles(rng, [g["name"] for g in docs["cluster"]["groups"]])
+    paths = _write_inputs(str(tmp_path), docs)
+    paths["profiles"] = str(tmp_path / "profiles.ndjson")
+    open(paths["profiles"], "w").write(text)
+    got = _run_plan(PLAN_B200, paths, str(tmp_path / "b200"))
+    want = _run_plan(PLAN_REF, paths, str(tmp_path / "ref"))
+    assert got[0] == want[0] == 0, (got[2], want[2])
+    assert got[2] == want[2] and "calibration" in want[2]
+    for k in want[3]:
+        assert got[3][k] == want[3][k], (cfg, k)
+    cal, diags = calibrate.calibrate_docs(docs, text)
+    assert [d for d in diags] == [line for line in want[2].splitlines() if line]
+    out = planner.search(cal)
+    p = abi.Problem(cal)
+    ref_plan = json.loads(want[3]["plan.json"])
+    assert abi.encode_plan(p.group_names, p.plan_from_doc(out.plan)) == abi.encode_plan(
+        p.group_names, p.plan_from_doc(ref_plan))
