@@ -9,6 +9,9 @@ from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libhetplan_b200.so")
+# tuning builds (tools/tune/) point this at an alternative in-tree build
+if os.environ.get("HP_LIB"):
+    SO = os.path.abspath(os.environ["HP_LIB"])
 
 _lib = None
 

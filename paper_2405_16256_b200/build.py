@@ -36,13 +36,15 @@ def needs_build() -> bool:
     return not os.path.exists(OUT) or os.path.getmtime(OUT) < _newest_dep_mtime()
 
 
-def build(verbose: bool = False, ptxas_v: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, ptxas_v: bool = False, out: str = OUT, defines=(), obj_dir: str = OBJ) -> str:
+    """defines: extra -D flags (tuning variants, tools/tune/); out/obj_dir
+    redirect a variant build away from the product library."""
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
 
     def compile_one(src):
-        obj = os.path.join(OBJ, src + ".o")
-        cmd = [NVCC, *ARCH, *COMMON, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(obj_dir, src + ".o")
+        cmd = [NVCC, *ARCH, *COMMON, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         if ptxas_v and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -54,11 +56,11 @@ def build(verbose: bool = False, ptxas_v: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         objs = list(ex.map(compile_one, srcs))
-    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs]
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

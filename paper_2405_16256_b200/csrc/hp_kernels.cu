@@ -60,7 +60,8 @@ struct Work {
 };
 
 __device__ __forceinline__ long long cand_id(const Work& w, int s) {
-  return w.ids ? w.ids[w.first + s] : w.first + s;
+  // ids may have been written by another SM (a leaf's step): read past L1
+  return w.ids ? __ldcg(w.ids + w.first + s) : w.first + s;
 }
 
 // Search-log sink (HP_FLAG_LOG). Kernels append, per decided batch, the
@@ -119,6 +120,10 @@ struct Bufs {
   const int* etbl_off;
   const int* ecap;
   LogSink log;
+  // neighbour screen (nb_screen): per-stage bound terms of each leaf's
+  // current split, and the surviving neighbour slots of its current step
+  StageLB* lbs;
+  long long* nb_ids;
 };
 
 // count of bounded compositions continuing with part value v at position j
@@ -597,10 +602,11 @@ struct AsyncQ {
   unsigned long long cap;
 };
 
-__device__ void push_items(const Bufs& b, const AsyncQ& q, int li, int cls, int level) {
+// Enqueues the n surviving neighbours (nb_ids of the leaf) of a leaf's
+// current step, cpw per item.
+__device__ void push_items(const Bufs& b, const AsyncQ& q, int li, int cls, int level, int nslots) {
   const Leaf lf = b.leaves[li];
   const int cpw = class_cpw(cls, lf.P);
-  const int nslots = 2 * (lf.P - 1);
   const int nit = (nslots + cpw - 1) / cpw;
   q.pending[li] = nit;
   unsigned long long t = atomicAdd(q.tail[level], (unsigned long long)nit);
@@ -619,14 +625,116 @@ __device__ void push_items(const Bufs& b, const AsyncQ& q, int li, int cls, int 
   }
 }
 
-// Enqueue the first step of every climbing leaf of class `cls`.
+// Whole warp: screens the neighbours of leaf li's current split (nb_screen;
+// off while the search log is recorded) and lists the survivors in nb_ids.
+// Screened slots get their T_SKIP / T_MEMORY / T_INVALID value in nb right
+// away. Returns the survivor count (warp-uniform).
+__device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane) {
+  const int P = lf.P;
+  const int nslots = 2 * (P - 1);
+  const LeafGroup* lg = b.lg + lf.lg_off;
+  const uint8_t* slots = b.layouts + lf.layout_off;
+  const double* hop = b.hop + lf.B_idx * c_consts.n_links;
+  const int* cur = b.cur + lf.split_off;
+  double* nbt = b.nb + b.nb_off[li];
+  long long* ids = b.nb_ids + b.nb_off[li];
+  StageLB* sl = b.lbs + lf.split_off;
+  const bool screen = b.log.vals == nullptr;
+  const double cur_t = b.hs[li].cur_time;
+  if (screen) {
+    for (int i = lane; i < P; i += 32) lb_stage(c_consts, lf, lg, slots, hop, i, cur[i], sl[i]);
+    __syncwarp();
+    if (lane == 0) lb_scan(lf, sl);
+    __syncwarp();
+  }
+  int n = 0;
+  for (int q0 = 0; q0 < nslots; q0 += 32) {
+    const int qq = q0 + lane;
+    bool surv = false;
+    if (qq < nslots) {
+      const double scr = screen ? nb_screen(c_consts, lf, lg, slots, hop, cur, sl, qq, cur_t) : 0.0;
+      if (scr == 0.0) surv = true;
+      else nbt[qq] = scr;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, surv);
+    if (surv) ids[n + __popc(m & ((1u << lane) - 1u))] = qq;
+    n += __popc(m);
+  }
+  __threadfence();
+  __syncwarp();
+  return n;
+}
+
+// Whole warp, after the last item of leaf li's step (do_step) or for its
+// first step: lane 0 runs the step (hill_step), then the warp screens the
+// next neighbourhood and enqueues the survivors. A neighbourhood with no
+// survivor cannot improve, so the next step runs at once (and stops).
+__device__ void advance_leaf(const Bufs& b, const AsyncQ& q, int li, int cls, int lane, bool do_step) {
+  const Leaf lf = b.leaves[li];
+  for (;;) {
+    if (do_step) {
+      int active = 0;
+      if (lane == 0) {
+        HillState hs = b.hs[li];
+        int delta[HP_MAX_STAGES];
+        unsigned char old[2 * HP_MAX_STAGES];
+        int tmp[HP_MAX_STAGES];
+        for (int i = 0; i < lf.P; ++i) delta[i] = 0;
+        const int seq = hs.steps;
+        hill_step(c_consts, lf, b.lg + lf.lg_off, b.layouts + lf.layout_off, b.cur + lf.split_off,
+                  b.uni + lf.split_off, b.prop + lf.split_off, b.best + lf.split_off,
+                  b.hist + b.hist_off[li], hs, b.nb + b.nb_off[li], delta, old, tmp);
+        b.hs[li] = hs;
+        if (b.log.vals) {  // simulated, non-memo neighbours in visit order (planner.cpp:472-476)
+          const double* nbt = b.nb + b.nb_off[li];
+          const int nslots = 2 * (lf.P - 1);
+          int n = 0;
+          for (int k = 0; k < nslots; ++k) n += (!old[k] && nbt[k] >= 0) ? 1 : 0;
+          long long off = log_reserve(b.log, li, seq, n);
+          if (off >= 0)
+            for (int k = 0; k < nslots; ++k)
+              if (!old[k] && nbt[k] >= 0) b.log.vals[off++] = nbt[k];
+        }
+        if (b.trace) {
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          unsigned long long k = atomicAdd(b.trace, 1ULL);
+          if (k < (1ULL << 22)) {
+            b.trace[1 + 2 * k] = now;
+            const unsigned long long mv = hs.steps > 0 ? (unsigned)b.hist[b.hist_off[li] + hs.steps - 1] : 0xfff;
+            b.trace[2 + 2 * k] = ((unsigned long long)cls << 56) | ((unsigned long long)(lf.P & 0xff) << 48) |
+                                 ((unsigned long long)(lf.M & 0xffff) << 32) | ((mv & 0xfff) << 20) |
+                                 (unsigned)(li & 0xfffff);
+          }
+        }
+        active = hs.active;
+        if (!active) {
+          __threadfence();
+          atomicSub(q.active, 1);
+        }
+      }
+      active = __shfl_sync(0xffffffffu, active, 0);
+      if (!active) return;
+      __syncwarp();
+    }
+    do_step = true;
+    const int n = screen_neighbours(b, li, lf, lane);
+    if (n > 0) {
+      if (lane == 0) push_items(b, q, li, cls, b.hs[li].steps >= kHiSteps ? 0 : 1, n);
+      return;
+    }
+  }
+}
+
+// Enqueue the first step of every climbing leaf of class `cls` (a warp per leaf).
 __global__ void k_async_seed(Bufs b, AsyncQ q, const int* ids, int n, int cls) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (k >= n) return;
-  int li = ids[k];
+  const int li = ids[k];
   if (!b.hs[li].active) return;
-  atomicAdd(q.active, 1);
-  push_items(b, q, li, cls, 1);
+  if (lane == 0) atomicAdd(q.active, 1);
+  advance_leaf(b, q, li, cls, lane, false);
 }
 
 __device__ __forceinline__ bool try_slot(const AsyncQ& q, int lv, long long& ticket, Work& w) {
@@ -677,8 +785,28 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[2]) {
   }
 }
 
+// Resident blocks of 256 threads per SM the hill-climb kernels are compiled
+// for (register cap 65536 / (256 * n)); more warps hide the FP64 latency of
+// the level chain. HP_MINB_K<K> overrides at build time (tuning).
+#ifndef HP_MINB_2
+#define HP_MINB_2 3
+#endif
+#ifndef HP_MINB_4
+#define HP_MINB_4 2
+#endif
+#ifndef HP_MINB_6
+#define HP_MINB_6 2
+#endif
+#ifndef HP_MINB_8
+#define HP_MINB_8 1
+#endif
 template <int K, bool FAST>
-__global__ void __launch_bounds__(256) k_hill_async(Bufs b, AsyncQ q, int cls) {
+constexpr int async_min_blocks() {
+  return !FAST ? 1 : (K == 2 ? HP_MINB_2 : K == 4 ? HP_MINB_4 : K == 6 ? HP_MINB_6 : HP_MINB_8);
+}
+
+template <int K, bool FAST>
+__global__ void __launch_bounds__(256, async_min_blocks<K, FAST>()) k_hill_async(Bufs b, AsyncQ q, int cls) {
   const int lane = threadIdx.x & 31;
   long long tk[2] = {-1, -1};
   for (;;) {
@@ -692,56 +820,17 @@ __global__ void __launch_bounds__(256) k_hill_async(Bufs b, AsyncQ q, int cls) {
     w.first = __shfl_sync(0xffffffffu, w.first, 0);
     w.n = __shfl_sync(0xffffffffu, w.n, 0);
     w.out = 0;
-    w.ids = nullptr;
+    w.ids = w.kind == 1 ? b.nb_ids + b.nb_off[w.leaf] : nullptr;
     eval_item<K, FAST>(b, w, lane);
     __syncwarp();
+    int last = 0;
     if (lane == 0) {
       __threadfence();
-      if (atomicSub(q.pending + w.leaf, 1) == 1) {
-        __threadfence();
-        const int li = w.leaf;
-        const Leaf lf = b.leaves[li];
-        HillState hs = b.hs[li];
-        int delta[HP_MAX_STAGES];
-        unsigned char old[2 * HP_MAX_STAGES];
-        int tmp[HP_MAX_STAGES];
-        for (int i = 0; i < lf.P; ++i) delta[i] = 0;
-        const int seq = hs.steps;
-        hill_step(c_consts, lf, b.lg + lf.lg_off, b.layouts + lf.layout_off, b.cur + lf.split_off,
-                  b.uni + lf.split_off, b.prop + lf.split_off, b.best + lf.split_off,
-                  b.hist + b.hist_off[li], hs, b.nb + b.nb_off[li], delta, old, tmp);
-        b.hs[li] = hs;
-        if (b.log.vals) {  // simulated, non-memo neighbours in visit order (planner.cpp:472-476)
-          const double* nbt = b.nb + b.nb_off[li];
-          const int nslots = 2 * (lf.P - 1);
-          int n = 0;
-          for (int q = 0; q < nslots; ++q) n += (!old[q] && nbt[q] >= 0) ? 1 : 0;
-          long long off = log_reserve(b.log, li, seq, n);
-          if (off >= 0)
-            for (int q = 0; q < nslots; ++q)
-              if (!old[q] && nbt[q] >= 0) b.log.vals[off++] = nbt[q];
-        }
-        if (b.trace) {
-          unsigned long long now;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-          unsigned long long k = atomicAdd(b.trace, 1ULL);
-          if (k < (1ULL << 22)) {
-            b.trace[1 + 2 * k] = now;
-            const unsigned long long mv = hs.steps > 0 ? (unsigned)b.hist[b.hist_off[li] + hs.steps - 1] : 0xfff;
-            b.trace[2 + 2 * k] = ((unsigned long long)cls << 56) | ((unsigned long long)(lf.P & 0xff) << 48) |
-                                 ((unsigned long long)(lf.M & 0xffff) << 32) | ((mv & 0xfff) << 20) |
-                                 (unsigned)(li & 0xfffff);
-          }
-        }
-        if (hs.active) {
-          __threadfence();
-          push_items(b, q, li, cls, hs.steps >= kHiSteps ? 0 : 1);
-        } else {
-          __threadfence();
-          atomicSub(q.active, 1);
-        }
-      }
+      last = atomicSub(q.pending + w.leaf, 1) == 1;
+      if (last) __threadfence();
     }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) advance_leaf(b, q, w.leaf, cls, lane, true);
     __syncwarp();
   }
 }
@@ -1005,7 +1094,9 @@ __global__ void __launch_bounds__(128) k_exh_thread(Bufs b, const ExhItem* items
   double bt = 0.0;
   long long brank = -1;
   int bcomp[P], comp[P];
-  long long sim = 0;
+  long long sim = 0, ran = 0;
+  const bool screen = b.log.exh == nullptr;  // the log needs every time
+  const double Md = (double)lf.M;
   if (cnt > 0) unrank_bounded_t<P>(r0, L, caps, tbl, comp);
   for (long long k = 0; k < cnt; ++k) {
     if (k) next_bounded_t<P>(comp, caps, sufcap);
@@ -1020,9 +1111,22 @@ __global__ void __launch_bounds__(128) k_exh_thread(Bufs b, const ExhItem* items
       bw[i] = layers * bl[i];
       dps[i] = dp_sync(row, comp[i]);
     }
+    ++sim;
+    if (screen && brank >= 0) {
+      // path lower bound (hp_search_core.cuh, nb_screen): a candidate above
+      // this thread's best can neither win nor tie, so it is not simulated
+      double A = 0.0, Bt = 0.0, lb = 0.0;
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        lb = dmax(lb, A + Md * (f[i] + bw[i]) + dmax(Bt + dps[0], dps[i]));
+        A = A + f[i] + sf[i];
+        Bt = Bt + sf[i] + bw[i];
+      }
+      if (lb > bt * (1.0 + kScreenMargin)) continue;
+    }
     const double t = sim_thread<P>(lf.M, f, bw, sf, sb, dps);
     if (b.log.exh) b.log.exh[b.log.exh_off[w.leaf] + r0 + k] = t;
-    ++sim;
+    ++ran;
     if (brank < 0 || t < bt || (t == bt && enc_less_t<P>(comp, bcomp))) {
       bt = t;
       brank = r0 + k;
@@ -1037,6 +1141,7 @@ __global__ void __launch_bounds__(128) k_exh_thread(Bufs b, const ExhItem* items
 #pragma unroll
     for (int i = 0; i < P; ++i) ocomp[i] = __shfl_xor_sync(0xffffffffu, bcomp[i], off);
     sim += __shfl_xor_sync(0xffffffffu, sim, off);
+    ran += __shfl_xor_sync(0xffffffffu, ran, off);
     const bool take = orank >= 0 && (brank < 0 || ot < bt || (ot == bt && enc_less_t<P>(ocomp, bcomp)));
     if (take) {
       bt = ot;
@@ -1047,7 +1152,7 @@ __global__ void __launch_bounds__(128) k_exh_thread(Bufs b, const ExhItem* items
   }
   if (lane == 0) {
     recs[it] = ExhRec{bt, brank, sim, w.leaf, brank >= 0 ? 1 : 0};
-    if (b.ops) atomicAdd(b.ops, (unsigned long long)sim * (unsigned long long)(8LL * P * lf.M - 4LL * lf.M));
+    if (b.ops) atomicAdd(b.ops, (unsigned long long)ran * (unsigned long long)(8LL * P * lf.M - 4LL * lf.M));
   }
 }
 
@@ -1344,6 +1449,8 @@ static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vect
   if (!(s = scratch(a, "hist", hist_total, &b.hist)).ok()) return s;
   if (!(s = scratch(a, "tseed", 2 * (size_t)nL, &b.tseed)).ok()) return s;
   if (!(s = scratch(a, "nb", nb_total, &b.nb)).ok()) return s;
+  if (!(s = scratch(a, "nb_ids", nb_total, &b.nb_ids)).ok()) return s;
+  if (!(s = scratch(a, "lbs", split_total, &b.lbs)).ok()) return s;
   if (!(s = scratch(a, "hs", nL, &b.hs)).ok()) return s;
   CK(cudaMemsetAsync(b.hs, 0, sizeof(HillState) * std::max(1, nL), st));
   return hph::Status{};
@@ -1558,7 +1665,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     reinterpret_cast<int*>(init + 5)[0] = grid * 8;  // warps of the launch
     CK(cudaMemcpyAsync(d_q, init, sizeof init, cudaMemcpyHostToDevice, ss));
     int n = static_cast<int>(by_cls[cls].size());
-    hpk::k_async_seed<<<(n + T - 1) / T, T, 0, ss>>>(b, q, d_cls_ids[cls], n, cls);
+    hpk::k_async_seed<<<(n * 32 + T - 1) / T, T, 0, ss>>>(b, q, d_cls_ids[cls], n, cls);
     launch_async(cls, b, q, grid, ss);
     out.launches += 2;
     out.eval_launches++;

@@ -10,6 +10,7 @@ namespace hpc {
 // Result codes stored per candidate slot.
 constexpr double T_INVALID = -2.0;   // neighbour with a count < 1 (planner.cpp:478)
 constexpr double T_MEMORY = -1.0;    // memory-pruned (planner.cpp:509-515)
+constexpr double T_SKIP = __builtin_huge_val();  // feasible, bound above the current time (nb_screen)
 
 // ------------------------------------------------------------ candidate setup
 
@@ -215,6 +216,106 @@ HPD bool next_bounded(int* c, int P, const int* caps, const int* sufcap) {
     suffix += c[j];
   }
   return false;
+}
+
+// ------------------------------------------------------------ neighbour screen
+//
+// An admissible lower bound on a candidate's iteration time, from one path
+// of the simulation DAG: F(0,0) -> F(1,0) -> ... -> F(k,0) (forward sends),
+// every op of stage k in order (2M ops), B(k,M-1) -> ... -> B(0,M-1)
+// (backward sends), then stage 0's DP sync; or stage k's own DP sync after
+// its last op. Each simulated node is max(predecessors) + duration and
+// rounding is monotone, so the simulated value of any node is >= the path
+// sum taken in path order, and the iteration time (a max over such nodes,
+// evaluate.cpp:90-97) is >= every path bound. Summation order here differs
+// from path order by far less than kScreenMargin (relative).
+//
+// A hill-climb neighbour whose bound exceeds the current point's time
+// (times (1 + margin)) can neither be the improving move (planner.cpp:
+// 479-487 needs t < current) nor tie the leaf best (best <= current), so it
+// need not be simulated: it is recorded as T_SKIP (+inf: feasible, counted as
+// simulated, never chosen). Decisions, counts and the winner are unchanged;
+// only the search log needs every time and turns the screen off.
+constexpr double kScreenMargin = 1e-6;
+
+// Per-stage terms of the current split (X_k, Y_k of the bound and their
+// prefix / suffix maxima).
+struct StageLB {
+  double f, b, sf, dps;  // durations of the current split
+  double A, Bt;          // sum_{i<k} (f_i + sf_i), sum_{i<k} (sf_i + b_i)
+  double PX, PY;         // max_{j<k} X_j, max_{j<k} Y_j
+  double SX, SY;         // max_{j>=k} X_j, max_{j>=k} Y_j
+};
+
+HPD double neg_inf() { return -__builtin_huge_val(); }
+
+// durations of stage i of the current split (feasible by construction)
+HPD void lb_stage(const Consts& c, const Leaf& lf, const LeafGroup* lg, const uint8_t* slots,
+                  const double* hop, int i, int count, StageLB& s) {
+  StageDur d;
+  stage_setup(c, lf, lg, slots, hop, i, count, d);
+  s.f = d.f;
+  s.b = d.b;
+  s.sf = d.sf;
+  s.dps = d.dps;
+}
+
+// X_k = A_k + M (f_k + b_k) + Bt_k (then + dps_0), Y_k = A_k + M (f_k + b_k) + dps_k
+HPD void lb_scan(const Leaf& lf, StageLB* s) {
+  const int P = lf.P;
+  const double M = (double)lf.M;
+  double A = 0.0, Bt = 0.0, px = neg_inf(), py = neg_inf();
+  for (int k = 0; k < P; ++k) {
+    s[k].A = A;
+    s[k].Bt = Bt;
+    s[k].PX = px;
+    s[k].PY = py;
+    const double core = A + M * (s[k].f + s[k].b);
+    const double X = core + Bt, Y = core + s[k].dps;
+    s[k].SX = X;
+    s[k].SY = Y;
+    px = dmax(px, X);
+    py = dmax(py, Y);
+    A = A + s[k].f + s[k].sf;
+    Bt = Bt + s[k].sf + s[k].b;
+  }
+  double sx = neg_inf(), sy = neg_inf();
+  for (int k = P - 1; k >= 0; --k) {
+    sx = dmax(sx, s[k].SX);
+    sy = dmax(sy, s[k].SY);
+    s[k].SX = sx;
+    s[k].SY = sy;
+  }
+}
+
+// Screens neighbour slot q of `cur` (boundary q >> 1, +1 for even q):
+// T_INVALID (a count < 1, planner.cpp:478), T_MEMORY (a changed stage fails
+// the memory gate; the others are the current split's), T_SKIP (bound above
+// cur_t), or 0.0 (must be simulated).
+HPD double nb_screen(const Consts& c, const Leaf& lf, const LeafGroup* lg, const uint8_t* slots,
+                     const double* hop, const int* cur, const StageLB* s, int q, double cur_t) {
+  const int P = lf.P;
+  const int bb = q >> 1;
+  const int dir = (q & 1) ? -1 : 1;
+  const int c0 = cur[bb] + dir, c1 = cur[bb + 1] - dir;
+  if (c0 < 1 || c1 < 1) return T_INVALID;
+  StageDur d0, d1;
+  const bool ok0 = stage_setup(c, lf, lg, slots, hop, bb, c0, d0);
+  const bool ok1 = stage_setup(c, lf, lg, slots, hop, bb + 1, c1, d1);
+  if (!ok0 || !ok1) return T_MEMORY;
+  const double M = (double)lf.M;
+  const double dps0 = bb == 0 ? d0.dps : s[0].dps;
+  double lb = dmax(s[bb].PX + dps0, s[bb].PY);  // k < bb (both -inf when bb == 0)
+  const double A0 = s[bb].A, B0 = s[bb].Bt;
+  lb = dmax(lb, A0 + M * (d0.f + d0.b) + dmax(B0 + dps0, d0.dps));
+  const double A1 = A0 + d0.f + s[bb].sf, B1 = B0 + s[bb].sf + d0.b;
+  lb = dmax(lb, A1 + M * (d1.f + d1.b) + dmax(B1 + dps0, d1.dps));
+  if (bb + 2 < P) {
+    const double dA = (d0.f - s[bb].f) + (d1.f - s[bb + 1].f);
+    const double dB = (d0.b - s[bb].b) + (d1.b - s[bb + 1].b);
+    lb = dmax(lb, dmax(s[bb + 2].SX + dA + dB + dps0, s[bb + 2].SY + dA));
+  }
+  return lb > cur_t * (1.0 + kScreenMargin) ? T_SKIP : 0.0;
 }
 
 // ------------------------------------------------------------ hill climb

@@ -52,6 +52,7 @@ def build_emu():
     lib = C.CDLL(EMU_SO)
     lib.emu_search.argtypes = [C.POINTER(abi.hp_problem), C.POINTER(abi.hp_result)]
     lib.emu_search_shard.argtypes = [C.POINTER(abi.hp_problem), C.c_int, C.c_int, C.POINTER(abi.hp_result)]
+    lib.emu_screen_stats.argtypes = [C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), C.c_int]
     return lib
 
 

@@ -16,6 +16,8 @@ using namespace hpc;
 
 namespace {
 
+long long g_screened = 0, g_neighbours = 0;  // nb_screen statistics (T_SKIP / all)
+
 struct LeafDev {
   Leaf lf;
   std::vector<LeafGroup> lg;
@@ -97,8 +99,19 @@ extern "C" int emu_search_shard(const hp_problem* in, int shard, int count, hp_r
       double tp = L.lf.mode == 2 ? -1 : eval(c, L, prop.data());
       hill_init(c, L.lf, L.lg.data(), L.slots, uni.data(), prop.data(), tu, tp, cur.data(), bs.data(),
                 hs, L.lf.mode == 2);
+      std::vector<StageLB> slb(P);
       while (hs.active) {
+        // the GPU's neighbour screen (nb_screen): only survivors are simulated
+        for (int i = 0; i < P; ++i) lb_stage(c, L.lf, L.lg.data(), L.slots, L.hop, i, cur[i], slb[i]);
+        lb_scan(L.lf, slb.data());
         for (int q = 0; q < 2 * (P - 1); ++q) {
+          double scr = nb_screen(c, L.lf, L.lg.data(), L.slots, L.hop, cur.data(), slb.data(), q, hs.cur_time);
+          g_neighbours++;
+          if (scr == T_SKIP) g_screened++;
+          if (scr != 0.0) {
+            nb[q] = scr;
+            continue;
+          }
           int b = q >> 1, d = (q & 1) ? -1 : 1;
           tmp = cur;
           tmp[b] += d; tmp[b + 1] -= d;
@@ -126,6 +139,12 @@ extern "C" int emu_search_shard(const hp_problem* in, int shard, int count, hp_r
 }
 
 extern "C" int emu_search(const hp_problem* in, hp_result* res) { return emu_search_shard(in, 0, 1, res); }
+
+extern "C" void emu_screen_stats(long long* screened, long long* neighbours, int reset) {
+  *screened = g_screened;
+  *neighbours = g_neighbours;
+  if (reset) g_screened = g_neighbours = 0;
+}
 
 // Explicit-plan evaluation through the same per-stage setup + serial
 // level-synchronous simulation (mode 3 pseudo-leaf, like hp_evaluate_plans).

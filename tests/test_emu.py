@@ -20,6 +20,11 @@ def full_cases(search_cases):
 
 
 def test_emu_matches_reference_full_mode(search_cases, emu):
+    """Includes the neighbour screen (nb_screen): neighbours whose path lower
+    bound exceeds the current time are not simulated; the C3 pp=12 case
+    screens out most of them and must still match the reference exactly."""
+    sk, nn = C.c_longlong(), C.c_longlong()
+    emu.emu_screen_stats(C.byref(sk), C.byref(nn), 1)
     n = 0
     for case in full_cases(search_cases):
         p = abi.Problem(case["docs"])
@@ -36,6 +41,8 @@ def test_emu_matches_reference_full_mode(search_cases, emu):
         assert abi.encode_plan(p.group_names, res.best_plan) == want, case["name"]
         n += 1
     assert n >= 60
+    emu.emu_screen_stats(C.byref(sk), C.byref(nn), 1)
+    assert sk.value > 0.3 * nn.value, (sk.value, nn.value)
 
 
 def test_emu_shards_partition_the_leaves(search_cases, emu):
