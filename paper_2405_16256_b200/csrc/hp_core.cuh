@@ -17,6 +17,15 @@
 #define HPD inline
 #endif
 
+// Load of per-leaf search state another SM may have written during the
+// same kernel (the hill climb's steps move between SMs): past L1 on the
+// device, a plain load in the CPU emulation.
+#if defined(__CUDA_ARCH__)
+#define HP_LDX(p) __ldcg(p)
+#else
+#define HP_LDX(p) (*(p))
+#endif
+
 namespace hpc {
 
 constexpr int MAXG = 8;      // device groups

@@ -115,7 +115,8 @@ struct Bufs {
   unsigned long long* ops;  // algorithmic FP64 add/max ops of simulated candidates
   // exhaustive regime: per-leaf bounded-composition tables (exh_table) and
   // memory caps; ranks of kind-2 work items index the bounded compositions
-  unsigned long long* trace;  // optional (HP_DEBUG_TRACE): [0] = count, then per-step (ns, leaf)
+  unsigned long long* trace;  // optional (HP_DEBUG_TRACE): [0] = count, then (ns, event) records
+  int trace_items;            // HP_DEBUG_TRACE_ITEMS: also item / screen / push events
   const long long* etbl;
   const int* etbl_off;
   const int* ecap;
@@ -123,7 +124,12 @@ struct Bufs {
   // neighbour screen (nb_screen): per-stage bound terms of each leaf's
   // current split, and the surviving neighbour slots of its current step
   StageLB* lbs;
+  StageNb* lbn;
   long long* nb_ids;
+  // memo distances of the climb: memo_d[hist_off + t] = ||S_k - S_t||_1
+  // between the current point k and path point t (prefix-sum space)
+  int* memo_d;
+  int nb_rows;  // kind-1 items are screened neighbours with StageLB/StageNb rows (full-mode climb)
 };
 
 // count of bounded compositions continuing with part value v at position j
@@ -170,14 +176,19 @@ __host__ __device__ inline int class_width(int cls, int P) {
   return cls < 4 ? (P + K - 1) / K : seg_width(P, K);
 }
 
-// Fast-kernel K maximising lane utilisation P*floor(32/W)/(32K), W = ceil(P/K).
+// Fast-kernel K maximising throughput: lane utilisation P*floor(32/W)/(32K),
+// W = ceil(P/K), times the core loop's rate at K stages per lane with the
+// climb kernel's 8 warps per SM (tools/micro/corebench: 6.4, 10.0, 11.5,
+// 11.2 T ops/s for K = 2..8 — more stages per lane is more independent FP64
+// work per warp, which at this occupancy hides the level's latency).
 __host__ __device__ inline int fast_K(int P) {
+  const double rate[4] = {6.4, 10.0, 11.5, 11.2};
   int bestK = 8;
   double bestU = -1.0;
   for (int K = 2; K <= 8; K += 2) {
     int W = (P + K - 1) / K;
     if (W > 32) continue;
-    double u = (double)P * (32 / W) / (32.0 * K);
+    double u = (double)P * (32 / W) / (32.0 * K) * rate[K / 2 - 1];
     if (u > bestU + 1e-12) {
       bestU = u;
       bestK = K;
@@ -356,6 +367,9 @@ __device__ __forceinline__ void eval_item_generic(const Bufs& b, const Work& w, 
 // the whole warp follows one instruction stream (no divergence) and only the
 // warm-up/cool-down windows are predicated. Segments are packed at exact
 // width W = ceil(P/K) (floor(32/W) candidates per warp).
+// Core-loop level pairs between early-abort checks of a screened neighbour.
+constexpr int kAbortPairs = 64;
+
 template <int K>
 __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, const int lane) {
   const Leaf lf = b.leaves[w.leaf];
@@ -397,26 +411,58 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
       if (r >= 0 && r < K) cnt[r] = v;
     }
   }
+  double dps[K];
+  if (w.kind == 1 && b.nb_rows) {
+    // screened neighbour (screen_neighbours): feasible, and its stage rows
+    // are the current split's (StageLB) except the two the move changes
+    // (StageNb at count -1 / +1)
+    const int q = has_cand ? (int)cand_id(w, seg) : 0;
+    const int mb = q >> 1, k0 = (q & 1) ? 0 : 1;
+    const StageLB* rl = b.lbs + lf.split_off;
+    const StageNb* rn = b.lbn + lf.split_off;
 #pragma unroll
-  for (int r = 0; r < K; ++r) {
-    const int i = sl * K + r;
-    f[r] = bw[r] = NEG;
-    sf[r] = 0.0;
-    if (has_cand && i < P) {
-      int c = w.kind == 2 ? cnt[r] : cand_count(b, lf, w, seg, i);
-      cnt[r] = c;
-      StageDur d;
-      if (c < 1) {
-        valid = false;
-      } else {
-        if (!stage_setup(c_consts, lf, lg, slots, hop, i, c, d)) mem_ok = false;
-        f[r] = d.f;
-        bw[r] = d.b;
-        // The last stage sends no activations forward and stage 0 no
-        // gradients backward (sim.cpp:127,137): a -inf hop keeps those
-        // channels at -inf, which doubles as the "no dependency" operand for
-        // the neighbouring segment / padding lanes (max(x, -inf) = x).
-        sf[r] = i == P - 1 ? NEG : d.sf;
+    for (int r = 0; r < K; ++r) {
+      const int i = sl * K + r;
+      f[r] = bw[r] = NEG;
+      sf[r] = 0.0;
+      dps[r] = 0.0;
+      if (has_cand && i < P) {
+        if (i == mb || i == mb + 1) {
+          const int k = i == mb ? k0 : 1 - k0;
+          f[r] = __ldcg(&rn[i].f[k]);
+          bw[r] = __ldcg(&rn[i].b[k]);
+          dps[r] = __ldcg(&rn[i].dps[k]);
+        } else {
+          f[r] = __ldcg(&rl[i].f);
+          bw[r] = __ldcg(&rl[i].b);
+          dps[r] = __ldcg(&rl[i].dps);
+        }
+        sf[r] = i == P - 1 ? NEG : __ldcg(&rl[i].sf);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int i = sl * K + r;
+      f[r] = bw[r] = NEG;
+      sf[r] = 0.0;
+      dps[r] = 0.0;
+      if (has_cand && i < P) {
+        int c = w.kind == 2 ? cnt[r] : cand_count(b, lf, w, seg, i);
+        StageDur d;
+        if (c < 1) {
+          valid = false;
+        } else {
+          if (!stage_setup(c_consts, lf, lg, slots, hop, i, c, d)) mem_ok = false;
+          f[r] = d.f;
+          bw[r] = d.b;
+          dps[r] = d.dps;
+          // The last stage sends no activations forward and stage 0 no
+          // gradients backward (sim.cpp:127,137): a -inf hop keeps those
+          // channels at -inf, which doubles as the "no dependency" operand for
+          // the neighbouring segment / padding lanes (max(x, -inf) = x).
+          sf[r] = i == P - 1 ? NEG : d.sf;
+        }
       }
     }
   }
@@ -445,6 +491,11 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
   // backward hop of the lane's first stage; stage 0 sends no gradient (-inf)
   const double sb_in = __shfl_sync(0xffffffffu, sf[K - 1], src_l);
   const double sb0 = sl == 0 ? NEG : sb_in;
+  // early-abort limit of a screened neighbour: the current point's time
+  const double lim = (w.kind == 1 && b.nb_rows) ? __ldcg(&b.hs[w.leaf].cur_time) * (1.0 + kScreenMargin)
+                                                : __builtin_huge_val();
+  bool dead = false;
+  int dead_t = 0;
   if (__any_sync(0xffffffffu, run)) {
     // ---- warm-up, levels 0..P-1: stage i runs F(i, t-i) once t >= i
     for (int t = 0; t < P; ++t) {
@@ -468,9 +519,14 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
     // stages always run opposite ops, so nothing needs a snapshot. PRED
     // levels (transition and cool-down windows) gate each op on its closed
     // form window with selects; core levels run every op unconditionally.
-    auto level = [&](auto par_tag, auto pred_tag, int t) {
+    // MODE 0: every op as simulate() does it; 1: the same and checks that no
+    // send waits for its channel (base_ok); 2: channel maxima dropped (see
+    // the core loop below).
+    bool base_ok = true;
+    auto level = [&](auto par_tag, auto pred_tag, auto mode_tag, int t) {
       constexpr int PAR = decltype(par_tag)::value;
       constexpr bool PRED = decltype(pred_tag)::value;
+      constexpr int MODE = decltype(mode_tag)::value;
       const double lchf = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
       const double rchb = __shfl_sync(0xffffffffu, chb[0], src_r);
       const int u0 = t + sl * K;  // t + i - r
@@ -480,7 +536,8 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
         if (((PAR - r) & 1) == 0) {
           const double recv = r == 0 ? lchf : chf[r > 0 ? r - 1 : 0];
           const double nfr = dmax(fr[r], recv) + f[r];
-          const double nch = dmax(nfr, chf[r]) + sf[r];
+          if (MODE == 1) base_ok = base_ok && !(chf[r] > nfr);
+          const double nch = (MODE == 2 ? nfr : dmax(nfr, chf[r])) + sf[r];
           if (PRED) {
             // F(i,m) at level 2m+i: 2P-i <= t <= 2M-2+i
             const bool act = (u0 + r >= 2 * P) && (v0 - r <= 2 * M - 2);
@@ -493,7 +550,8 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
         } else {
           const double recv = r == K - 1 ? rchb : chb[r < K - 1 ? r + 1 : 0];
           const double nfr = dmax(fr[r], recv) + bw[r];
-          const double nch = dmax(nfr, chb[r]) + (r == 0 ? sb0 : sf[r > 0 ? r - 1 : 0]);
+          if (MODE == 1) base_ok = base_ok && !(chb[r] > nfr);
+          const double nch = (MODE == 2 ? nfr : dmax(nfr, chb[r])) + (r == 0 ? sb0 : sf[r > 0 ? r - 1 : 0]);
           if (PRED) {
             // B(i,j) at level 2P-1-i+2j: 2P-1-i <= t <= 2M+2P-3-i
             const bool act = (u0 + r >= 2 * P - 1) && (u0 + r <= 2 * M + 2 * P - 3);
@@ -510,20 +568,111 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
     using I1 = std::integral_constant<int, 1>;
     using PT = std::true_type;
     using PF = std::false_type;
+    using M0 = std::integral_constant<int, 0>;
+    using M1 = std::integral_constant<int, 1>;
+    using M2 = std::integral_constant<int, 2>;
     auto pred_level = [&](int t) {
-      if (t & 1) level(I1{}, PT{}, t);
-      else level(I0{}, PT{}, t);
+      if (t & 1) level(I1{}, PT{}, M0{}, t);
+      else level(I0{}, PT{}, M0{}, t);
     };
     int t = P;
     for (; t < T && t < core_lo; ++t) pred_level(t);
     if (core_lo <= core_hi) {
-      // core_lo is even: pairs (even, odd), then the final even level
-      for (; t + 1 <= core_hi; t += 2) {
-        level(I0{}, PF{}, t);
-        level(I1{}, PF{}, t + 1);
+      // core_lo is even: pairs (even, odd), then the final even level.
+      // Channel maxima: in the core every stage alternates F and B, so
+      // between two forwards of stage i there is a backward and
+      // F_end(m+1) >= fl(fl(F_end(m) + b) + f). If send(m) did not wait
+      // (its channel end is F_end(m) + sf) and sf < f + b by more than the
+      // rounding of those adds, send(m+1) cannot wait either: the channel
+      // max is max(F_end, ...) = F_end, exactly. Same for backward sends
+      // (sb < f + b). So after a first pair that checks every send of the
+      // core starts without waiting (MODE 1), the channel maxima are no-ops
+      // and are dropped (MODE 2). The rounding slack is 4 ulps of an upper
+      // bound on every node value: M * sum over stages of (f + b + sf + sb).
+      bool chok = true;
+      {
+        double vs = 0.0;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const int i = sl * K + r;
+          if (run && i < P) {
+            const double sbk = r == 0 ? sb0 : sf[r > 0 ? r - 1 : 0];
+            vs = vs + (f[r] + bw[r]) + (dmax(sf[r], 0.0) + dmax(sbk, 0.0));
+          }
+        }
+        for (int off = 1; off < W; off <<= 1) {
+          const double o = __shfl_down_sync(0xffffffffu, vs, off);
+          if (sl + off < W) vs = vs + o;
+        }
+        vs = __shfl_sync(0xffffffffu, vs, min(31, seg * W));
+        const double slack = vs * (double)M * 0x1p-50;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const int i = sl * K + r;
+          if (run && i < P) {
+            const double sbk = r == 0 ? sb0 : sf[r > 0 ? r - 1 : 0];
+            const double fb = (f[r] + bw[r]) - slack;
+            chok = chok && sf[r] < fb && sbk < fb;
+          }
+        }
+      }
+      bool noch = false;
+      if (t + 1 <= core_hi) {
+        level(I0{}, PF{}, M1{}, t);
+        level(I1{}, PF{}, M1{}, t + 1);
+        t += 2;
+        noch = __all_sync(0xffffffffu, !run || (chok && base_ok));
+      }
+      // Every kAbortPairs pairs a screened neighbour checks the bound below.
+      for (; t + 1 <= core_hi;) {
+        const int stop = min(core_hi - 1, t + 2 * kAbortPairs - 2);
+        if (noch) {
+          for (; t <= stop; t += 2) {
+            level(I0{}, PF{}, M2{}, t);
+            level(I1{}, PF{}, M2{}, t + 1);
+          }
+        } else {
+          for (; t <= stop; t += 2) {
+            level(I0{}, PF{}, M0{}, t);
+            level(I1{}, PF{}, M0{}, t + 1);
+          }
+        }
+        if (lim < __builtin_huge_val()) {
+          // Early abort: levels < t are done; stage i has issued
+          // nF = (t-1-i)/2 + 1 forwards and nB = (t-2P+i)/2 + 1 backwards
+          // (closed form above, every stage past its warm-up). Its remaining
+          // ops run in order after fr, so compute_end_i + dp_sync_i >=
+          // fr + (M-nF) f + (M-nB) b + dps (rounding is monotone; the
+          // margin absorbs the summation order), a lower bound on the
+          // iteration time (evaluate.cpp:90-97). A neighbour above the
+          // current point's time can neither be the move nor tie the leaf
+          // best (nb_screen), so it stops here as T_SKIP.
+          double lb = NEG;
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const int i = sl * K + r;
+            if (run && i < P) {
+              const int nf = min(M, (t - 1 - i) / 2 + 1), nbk = min(M, (t - 2 * P + i) / 2 + 1);
+              lb = dmax(lb, fr[r] + ((double)(M - nf) * f[r] + (double)(M - nbk) * bw[r]) + dps[r]);
+            }
+          }
+          for (int off = 1; off < W; off <<= 1) {
+            const double o = __shfl_down_sync(0xffffffffu, lb, off);
+            if (sl + off < W) lb = dmax(lb, o);
+          }
+          lb = __shfl_sync(0xffffffffu, lb, min(31, seg * W));
+          if (run && !dead && lb > lim) {
+            dead = true;
+            dead_t = t;
+          }
+          if (__all_sync(0xffffffffu, dead || !run)) {
+            t = T;  // every candidate of the warp is out
+            break;
+          }
+        }
       }
       if (t <= core_hi) {
-        level(I0{}, PF{}, t);
+        level(I0{}, PF{}, M0{}, t);
         ++t;
       }
     }
@@ -537,7 +686,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
       v = dmax(v, fr[r]);
       v = dmax(v, chf[r]);
       v = dmax(v, chb[r]);
-      v = dmax(v, fr[r] + dp_sync(lg[slots[i]], cnt[r]));
+      v = dmax(v, fr[r] + dps[r]);
     }
   }
   for (int off = 1; off < W; off <<= 1) {
@@ -545,11 +694,13 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
     if (sl + off < W) v = dmax(v, o);
   }
   if (sl == 0 && has_cand) {
-    double tt = inv ? T_INVALID : (mem ? T_MEMORY : v);
+    double tt = inv ? T_INVALID : (mem ? T_MEMORY : (dead ? T_SKIP : v));
     if (w.kind == 0) b.tseed[2 * w.leaf + (int)cand_id(w, seg)] = tt;
     else if (w.kind == 1) b.nb[b.nb_off[w.leaf] + (int)cand_id(w, seg)] = tt;
     else b.xbuf[w.out + seg] = tt;
-    if (run && b.ops) atomicAdd(b.ops, (unsigned long long)(8LL * P * M - 4LL * M));
+    // algorithmic ops of the levels this candidate needed
+    const long long full = 8LL * P * M - 4LL * M;
+    if (run && b.ops) atomicAdd(b.ops, (unsigned long long)(dead ? full * dead_t / (2LL * (M + P - 1)) : full));
   }
 }
 
@@ -580,48 +731,188 @@ __global__ void __launch_bounds__(256) k_eval(Bufs b, const Work* items, const i
 // leaf advances on its own: the warp that finishes the last neighbour item of
 // a leaf runs that leaf's step (hill_step) and enqueues its next neighbours,
 // so there is no global per-step barrier and no host round trip; the kernel
-// ends when no leaf of its class is still climbing.
+// ends when no leaf is still climbing. One persistent kernel serves every
+// evaluator class (the item's leaf selects the evaluator), so the long climbs
+// of one class overlap the bulk of the others instead of forming a serial
+// tail per class.
 // Two FIFO rings with ticket claims: level 0 (priority) receives the steps
-// of leaves that have already made kHiSteps moves — long climbers are the
-// critical path of a class, so their items should not wait behind a full
-// round of every other leaf's items — level 1 everything else. Each warp
+// of the critical leaves — the host's pick of the longest expected climbs
+// (P^2 M), as many as keep the ring within the resident warps, plus any leaf
+// whose climb so far is long (steps x levels per simulation >= hi_levels) —
+// level 1 everything else. The long climbs are the critical path: a step
+// waits for all of its items, so a climb behind a full ring advances one
+// ring's worth of items per step. Priority items run the lowest-latency
+// evaluator for their P (K = 4 up to P = 128: fewer stages per lane, a
+// shorter level) rather than the densest one. Each warp
 // holds at most one ticket per ring; it claims a priority ticket only when
 // the priority ring has unclaimed items, serves whichever of its tickets is
 // filled first, and keeps them across items (no CAS loops, no contention).
-constexpr int kHiSteps = 8;
-
 struct AsyncQ {
   Work* slots[2];
   unsigned long long* seq[2];   // slot k holds ticket t when seq[k] == t + 1
   unsigned long long* head[2];  // next ticket to hand out
   unsigned long long* tail[2];  // next ticket to produce
   int* pending;                 // per leaf: items of the current step not yet done
-  int* active;                  // leaves of this class still climbing
-  int* abort;                   // watchdog flag (shared by all classes)
-  int* live;                    // resident warps of this class's kernel
+  int* active;                  // leaves still climbing
+  int* abort;                   // watchdog flag
   unsigned long long cap;
+  long long hi_levels;          // priority threshold (see above)
+  const unsigned char* crit;    // per leaf: critical (level 0 from the first step)
+  int lat;                      // level-0 items use lat_class
 };
 
-// Enqueues the n surviving neighbours (nb_ids of the leaf) of a leaf's
-// current step, cpw per item.
-__device__ void push_items(const Bufs& b, const AsyncQ& q, int li, int cls, int level, int nslots) {
-  const Leaf lf = b.leaves[li];
+__device__ __forceinline__ int leaf_class(const Leaf& lf) { return eval_class(lf.P, lf.M, lf.sched == 0); }
+
+// Lowest-latency fast class for a leaf (see AsyncQ); generic leaves keep theirs.
+__host__ __device__ inline int lat_class(int P, int cls) {
+  if (cls >= 4) return cls;
+  return P <= 128 ? 1 : (P <= 192 ? 2 : 3);
+}
+
+// HP_DEBUG_TRACE record: (globaltimer ns, ev << 59 | cls << 56 | P << 48 |
+// M << 32 | aux << 20 | leaf). ev 0: step done (aux = move), 1: item
+// start, 2: item end, 3: neighbourhood screened (aux = survivors), 4: items
+// pushed.
+__device__ void trace_event(const Bufs& b, int ev, int li, const Leaf& lf, unsigned aux) {
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  unsigned long long k = atomicAdd(b.trace, 1ULL);
+  if (k < (1ULL << 22)) {
+    b.trace[1 + 2 * k] = now;
+    b.trace[2 + 2 * k] = ((unsigned long long)ev << 59) | ((unsigned long long)leaf_class(lf) << 56) |
+                         ((unsigned long long)(lf.P & 0xff) << 48) | ((unsigned long long)(lf.M & 0xffff) << 32) |
+                         ((unsigned long long)(aux & 0xfff) << 20) | (unsigned)(li & 0xfffff);
+  }
+}
+
+// Whole warp: enqueues the n surviving neighbours (nb_ids of the leaf) of a
+// leaf's current step, cpw per item, one item per lane.
+__device__ void push_items(const Bufs& b, const AsyncQ& q, int li, const Leaf& lf, int level, int nslots,
+                           int lane) {
+  const int cls = level == 0 && q.lat ? lat_class(lf.P, leaf_class(lf)) : leaf_class(lf);
   const int cpw = class_cpw(cls, lf.P);
   const int nit = (nslots + cpw - 1) / cpw;
-  q.pending[li] = nit;
-  unsigned long long t = atomicAdd(q.tail[level], (unsigned long long)nit);
-  for (int j = 0; j < nit; ++j) {
-    Work w;
-    w.leaf = li;
-    w.kind = 1;
-    w.first = j * cpw;
-    w.n = min(cpw, nslots - j * cpw);
-    w.out = 0;
-    w.ids = nullptr;
-    const unsigned long long k = (t + j) % q.cap;
-    q.slots[level][k] = w;
+  unsigned long long t = 0;
+  if (lane == 0) {
+    q.pending[li] = nit;
+    __threadfence();  // pending is set before any item of the step is visible
+    t = atomicAdd(q.tail[level], (unsigned long long)nit);
+  }
+  t = __shfl_sync(0xffffffffu, t, 0);
+  for (int j0 = 0; j0 < nit; j0 += 32) {
+    const int j = j0 + lane;
+    unsigned long long k = 0;
+    if (j < nit) {
+      Work w;
+      w.leaf = li;
+      w.kind = 1;
+      w.first = j * cpw;
+      w.n = min(cpw, nslots - j * cpw);
+      w.out = cls + 1;  // evaluator class + 1 (kind-1 items have no output slot)
+      w.ids = nullptr;
+      k = (t + j) % q.cap;
+      q.slots[level][k] = w;
+    }
     __threadfence();
-    atomicExch(q.seq[level] + k, t + j + 1);
+    if (j < nit) atomicExch(q.seq[level] + k, t + j + 1);
+  }
+}
+
+// Warp scans over per-stage values held in contiguous chunks of C stages
+// per lane (lane l: stages [l*C, l*C+C)). Exclusive prefix sum / prefix max
+// and inclusive-from-the-right suffix max of the lanes' chunk totals.
+__device__ __forceinline__ double warp_excl_sum(double v, int lane) {
+  double x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = x + y;
+  }
+  const double e = __shfl_up_sync(0xffffffffu, x, 1);
+  return lane == 0 ? 0.0 : e;
+}
+__device__ __forceinline__ double warp_excl_max(double v, int lane) {
+  double x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = dmax(x, y);
+  }
+  const double e = __shfl_up_sync(0xffffffffu, x, 1);
+  return lane == 0 ? neg_inf() : e;
+}
+__device__ __forceinline__ double warp_excl_suffix_max(double v, int lane) {
+  double x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_down_sync(0xffffffffu, x, o);
+    if (lane + o < 32) x = dmax(x, y);
+  }
+  const double e = __shfl_down_sync(0xffffffffu, x, 1);
+  return lane == 31 ? neg_inf() : e;
+}
+
+// lb_scan (hp_search_core.cuh) across the warp: the prefix sums are added in
+// a different order than the path, which kScreenMargin absorbs.
+__device__ void lb_scan_warp(const Leaf& lf, StageLB* s, int lane) {
+  const int P = lf.P;
+  const int C = (P + 31) >> 5;
+  const int i0 = min(P, lane * C), i1 = min(P, i0 + C);
+  const double M = (double)lf.M;
+  double sa = 0.0, sb = 0.0;
+  double f[8], bk[8], sf[8], dps[8];  // the lane's chunk (C <= 8)
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + r;
+    if (i < i1) {
+      f[r] = __ldcg(&s[i].f);
+      bk[r] = __ldcg(&s[i].b);
+      sf[r] = __ldcg(&s[i].sf);
+      dps[r] = __ldcg(&s[i].dps);
+      sa = sa + f[r] + sf[r];
+      sb = sb + sf[r] + bk[r];
+    }
+  }
+  double A = warp_excl_sum(sa, lane), Bt = warp_excl_sum(sb, lane);
+  double mx = neg_inf(), my = neg_inf();
+  double X[8], Y[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + r;
+    if (i < i1) {
+      __stcg(&s[i].A, A);
+      __stcg(&s[i].Bt, Bt);
+      const double core = A + M * (f[r] + bk[r]);
+      X[r] = core + Bt;
+      Y[r] = core + dps[r];
+      mx = dmax(mx, X[r]);
+      my = dmax(my, Y[r]);
+      A = A + f[r] + sf[r];
+      Bt = Bt + sf[r] + bk[r];
+    }
+  }
+  double px = warp_excl_max(mx, lane), py = warp_excl_max(my, lane);
+  const double qx = warp_excl_suffix_max(mx, lane), qy = warp_excl_suffix_max(my, lane);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + r;
+    if (i < i1) {
+      __stcg(&s[i].PX, px);
+      __stcg(&s[i].PY, py);
+      px = dmax(px, X[r]);
+      py = dmax(py, Y[r]);
+    }
+  }
+  double sx = qx, sy = qy;
+#pragma unroll
+  for (int r = 7; r >= 0; --r) {
+    const int i = i0 + r;
+    if (i < i1) {
+      sx = dmax(sx, X[r]);
+      sy = dmax(sy, Y[r]);
+      __stcg(&s[i].SX, sx);
+      __stcg(&s[i].SY, sy);
+    }
   }
 }
 
@@ -629,7 +920,7 @@ __device__ void push_items(const Bufs& b, const AsyncQ& q, int li, int cls, int 
 // off while the search log is recorded) and lists the survivors in nb_ids.
 // Screened slots get their T_SKIP / T_MEMORY / T_INVALID value in nb right
 // away. Returns the survivor count (warp-uniform).
-__device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane) {
+__device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane, int moved) {
   const int P = lf.P;
   const int nslots = 2 * (P - 1);
   const LeafGroup* lg = b.lg + lf.lg_off;
@@ -639,12 +930,42 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
   double* nbt = b.nb + b.nb_off[li];
   long long* ids = b.nb_ids + b.nb_off[li];
   StageLB* sl = b.lbs + lf.split_off;
+  StageNb* sn = b.lbn + lf.split_off;
   const bool screen = b.log.vals == nullptr;
-  const double cur_t = b.hs[li].cur_time;
+  const double cur_t = __ldcg(&b.hs[li].cur_time);
   if (screen) {
-    for (int i = lane; i < P; i += 32) lb_stage(c_consts, lf, lg, slots, hop, i, cur[i], sl[i]);
+    // (cur was last written by whichever SM ran the previous step)
+    // per-stage rows: all stages on the first step, afterwards only the two
+    // stages the last move changed (moved, moved + 1)
+    if (moved < 0) {
+      const int C = (P + 31) >> 5;
+      const int i1 = min(P, lane * C + C);
+      for (int i = lane * C; i < i1; ++i) {
+        const int ci = __ldcg(cur + i);
+        lb_stage(c_consts, lf, lg, slots, hop, i, ci, sl[i]);
+        lb_stage_nb(c_consts, lf, lg, slots, hop, i, ci, sn[i]);
+      }
+    } else if (lane < 2) {
+      const int i = moved + lane;
+      const int ci = __ldcg(cur + i);
+      StageLB t;
+      lb_stage(c_consts, lf, lg, slots, hop, i, ci, t);
+      __stcg(&sl[i].f, t.f);
+      __stcg(&sl[i].b, t.b);
+      __stcg(&sl[i].sf, t.sf);
+      __stcg(&sl[i].dps, t.dps);
+      StageNb u;
+      lb_stage_nb(c_consts, lf, lg, slots, hop, i, ci, u);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        __stcg(&sn[i].f[k], u.f[k]);
+        __stcg(&sn[i].b[k], u.b[k]);
+        __stcg(&sn[i].dps[k], u.dps[k]);
+        __stcg(&sn[i].st[k], u.st[k]);
+      }
+    }
     __syncwarp();
-    if (lane == 0) lb_scan(lf, sl);
+    lb_scan_warp(lf, sl, lane);
     __syncwarp();
   }
   int n = 0;
@@ -652,7 +973,7 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
     const int qq = q0 + lane;
     bool surv = false;
     if (qq < nslots) {
-      const double scr = screen ? nb_screen(c_consts, lf, lg, slots, hop, cur, sl, qq, cur_t) : 0.0;
+      const double scr = screen ? nb_screen_pre(lf, sl, sn, qq, cur_t) : 0.0;
       if (scr == 0.0) surv = true;
       else nbt[qq] = scr;
     }
@@ -665,27 +986,302 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
   return n;
 }
 
+// Whole warp: hill_step (hp_search_core.cuh, planner.cpp:470-489) with the
+// memo scan and the neighbour loop spread over the lanes; same decisions,
+// counts and leaf best. Boundary bb (slots 2bb, 2bb+1) belongs to lane
+// bb & 31, register k = bb >> 5. Returns hs.active.
+__device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, int& moved) {
+  const unsigned FULL = 0xffffffffu;
+  const int P = lf.P;
+  const int nslots = 2 * (P - 1);
+  int* cur = b.cur + lf.split_off;
+  int* best = b.best + lf.split_off;
+  short* hist = b.hist + b.hist_off[li];
+  const double* nb = b.nb + b.nb_off[li];
+  HillState hs;
+  hs.cur_time = __ldcg(&b.hs[li].cur_time);
+  hs.best_time = __ldcg(&b.hs[li].best_time);
+  hs.steps = __ldcg(&b.hs[li].steps);
+  hs.has_best = __ldcg(&b.hs[li].has_best);
+  constexpr int NK = (HP_MAX_STAGES + 31) / 32;
+
+  // ---- mark_old (hp_search_core.cuh): path points t with D_t = ||S_k - S_t||_1
+  // <= 2 (memo_d, maintained incrementally below). For those the nonzero
+  // boundaries of S_k - S_t come from undoing moves k-1..t (rare beyond t =
+  // k-2 on a strictly improving path).
+  int* memo = b.memo_d + b.hist_off[li];
+  unsigned oldm = 0;  // bit 2k + (dir < 0) for my boundary lane + 32k
+  bool all_old = false;
+  for (int t0 = hs.steps - 1; t0 >= 0; t0 -= 32) {
+    const int idx = t0 - lane;
+    const int dv = idx >= 0 ? __ldcg(memo + idx) : 3;
+    unsigned fl = __ballot_sync(FULL, dv <= 2);
+    while (fl) {
+      const int j = __ffs(fl) - 1;
+      fl &= fl - 1;
+      const int t = t0 - j;
+      if (__shfl_sync(FULL, dv, j) == 0) {
+        all_old = true;
+        continue;
+      }
+      int dl[NK];
+#pragma unroll
+      for (int k = 0; k < NK; ++k) dl[k] = 0;
+      for (int u = hs.steps - 1; u >= t; --u) {
+        const int code = __ldcg(hist + u);
+        const int bb = code >> 1;
+        if ((bb & 31) == lane) {
+          const int r = bb >> 5;
+#pragma unroll
+          for (int k = 0; k < NK; ++k)
+            if (k == r) dl[k] += (code & 1) ? -1 : 1;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NK; ++k)
+        if (dl[k] != 0) oldm |= 1u << (2 * k + (dl[k] > 0 ? 1 : 0));  // toward c_t
+    }
+  }
+  // seeds at distance 1: prefix sums of cur - ref over each lane's chunk
+  {
+    const int C = (P + 31) >> 5;
+    const int i0 = min(P, lane * C), i1 = min(P, i0 + C);
+    for (int sd = 0; sd < 2; ++sd) {
+      const int* ref = (sd == 0 ? b.uni : b.prop) + lf.split_off;
+      int loc = 0;
+      for (int i = i0; i < i1; ++i) loc += __ldcg(cur + i) - ref[i];
+      int x = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      int e = __shfl_up_sync(FULL, x, 1);
+      if (lane == 0) e = 0;
+      int dist = 0, cb = -1, cd = 0;
+      for (int i = i0; i < i1 && i + 1 < P; ++i) {
+        e += __ldcg(cur + i) - ref[i];
+        if (e != 0) {
+          dist += abs(e);
+          cb = i;
+          cd = e;
+        }
+      }
+      dist = __reduce_add_sync(FULL, dist);
+      if (dist == 1) {  // one boundary at distance 1: move its bit to the owner lane
+        const int src = __ffs(__ballot_sync(FULL, cb >= 0)) - 1;
+        const int gb = __shfl_sync(FULL, cb, src);
+        const int gd = __shfl_sync(FULL, cd, src);
+        if ((gb & 31) == lane) oldm |= 1u << (2 * (gb >> 5) + (gd > 0 ? 1 : 0));
+      }
+    }
+  }
+
+  // ---- neighbour loop: counts, move argmin (time, slot), best candidate
+  long long sim = 0, pru = 0;
+  double mt = __builtin_huge_val();
+  int mq = 0x7fffffff;                 // feasible argmin (first slot on ties)
+  double nt = __builtin_huge_val();
+  int nq = 0x7fffffff, ntie = 0;       // non-old feasible minimum
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    const int bb = lane + 32 * k;
+    if (bb + 1 < P) {
+#pragma unroll
+      for (int sd = 0; sd < 2; ++sd) {
+        const int q = 2 * bb + sd;
+        const double t = __ldcg(nb + q);
+        if (t == T_INVALID) continue;
+        const bool old = all_old || ((oldm >> (2 * k + sd)) & 1u);
+        if (!old) {
+          if (t >= 0) ++sim;
+          else ++pru;
+        }
+        if (t < 0) continue;
+        if (t < mt || (t == mt && q < mq)) {
+          mt = t;
+          mq = q;
+        }
+        if (!old) {
+          if (t < nt || (t == nt && q < nq)) {
+            if (t < nt) ntie = 0;
+            nt = t;
+            nq = q;
+          }
+          if (t == nt) ++ntie;
+        }
+      }
+    }
+  }
+  sim = __reduce_add_sync(FULL, (unsigned)sim);
+  pru = __reduce_add_sync(FULL, (unsigned)pru);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t2 = __shfl_xor_sync(FULL, mt, o);
+    const int q2 = __shfl_xor_sync(FULL, mq, o);
+    if (t2 < mt || (t2 == mt && q2 < mq)) {
+      mt = t2;
+      mq = q2;
+    }
+    const double u2 = __shfl_xor_sync(FULL, nt, o);
+    const int r2 = __shfl_xor_sync(FULL, nq, o);
+    const int c2 = __shfl_xor_sync(FULL, ntie, o);
+    if (u2 < nt) {
+      nt = u2;
+      nq = r2;
+      ntie = c2;
+    } else if (u2 == nt) {
+      ntie += c2;
+      nq = min(nq, r2);
+    }
+  }
+  // leaf best: the minimum of (best, non-old feasible neighbours) in the
+  // (time, encoding) order; ties in time need the encodings (rare: serial)
+  const bool have_n = nq != 0x7fffffff;
+  bool serial_best = false;
+  bool take_n = false;
+  if (have_n) {
+    if (!hs.has_best || nt < hs.best_time) {
+      if (ntie == 1) take_n = true;
+      else serial_best = true;
+    } else if (nt == hs.best_time) {
+      serial_best = true;
+    }
+  }
+  if (serial_best) {
+    // slot old flags to scratch (nb_ids is rewritten by the next screen)
+    unsigned char* oldb = reinterpret_cast<unsigned char*>(b.nb_ids + b.nb_off[li]);
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+      const int bb = lane + 32 * k;
+      if (bb + 1 < P) {
+        oldb[2 * bb] = all_old || ((oldm >> (2 * k)) & 1u);
+        oldb[2 * bb + 1] = all_old || ((oldm >> (2 * k + 1)) & 1u);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      int cl[HP_MAX_STAGES], bl[HP_MAX_STAGES], tmp[HP_MAX_STAGES];
+      for (int i = 0; i < P; ++i) {
+        cl[i] = __ldcg(cur + i);
+        bl[i] = __ldcg(best + i);
+      }
+      for (int q = 0; q < nslots; ++q) {
+        const double t = __ldcg(nb + q);
+        if (t < 0 || oldb[q]) continue;
+        bool better = !hs.has_best || t < hs.best_time;
+        const int bq = q >> 1, d = (q & 1) ? -1 : 1;
+        if (!better && t == hs.best_time) {
+          for (int i = 0; i < P; ++i) tmp[i] = cl[i];
+          tmp[bq] += d;
+          tmp[bq + 1] -= d;
+          better = split_enc_less(P, tmp, bl);
+        }
+        if (better) {
+          hs.has_best = 1;
+          hs.best_time = t;
+          for (int i = 0; i < P; ++i) bl[i] = cl[i];
+          bl[bq] += d;
+          bl[bq + 1] -= d;
+        }
+      }
+      for (int i = 0; i < P; ++i) __stcg(best + i, bl[i]);
+    }
+    __syncwarp();
+  } else if (take_n) {
+    const int bq = nq >> 1, d = (nq & 1) ? -1 : 1;
+    for (int i = lane; i < P; i += 32) __stcg(best + i, __ldcg(cur + i) + (i == bq ? d : (i == bq + 1 ? -d : 0)));
+    hs.has_best = 1;
+    hs.best_time = nt;
+  }
+  __syncwarp();
+  int active = 1;
+  if (lane == 0) {
+    HillState& g = b.hs[li];
+    __stcg(&g.simulated, __ldcg(&g.simulated) + sim);
+    __stcg(&g.pruned, __ldcg(&g.pruned) + pru);
+    __stcg(&g.has_best, hs.has_best);
+    __stcg(&g.best_time, hs.best_time);
+    if (mq == 0x7fffffff || !(mt < hs.cur_time)) {  // no feasible neighbour, or no improvement
+      active = 0;
+    } else {
+      const int bq = mq >> 1, d = (mq & 1) ? -1 : 1;
+      __stcg(cur + bq, __ldcg(cur + bq) + d);
+      __stcg(cur + bq + 1, __ldcg(cur + bq + 1) - d);
+      __stcg(hist + hs.steps, (short)mq);
+      __stcg(&g.steps, hs.steps + 1);
+      __stcg(&g.cur_time, mt);
+      if (hs.steps + 1 >= 4 * c_consts.L) active = 0;
+    }
+    __stcg(&g.active, active);
+  }
+  active = __shfl_sync(FULL, active, 0);
+  moved = mq >> 1;
+  if (active) {
+    // D_t(k+1) = D_t(k) + |c(t) + d| - |c(t)|, c(t) = sum of the moves of
+    // boundary mb over t..k-1 (a suffix scan, 32 path points per round);
+    // D_k(k+1) = 1
+    const int mb = mq >> 1, md = (mq & 1) ? -1 : 1;
+    int carry = 0;
+    for (int t0 = hs.steps - 1; t0 >= 0; t0 -= 32) {
+      const int idx = t0 - lane;
+      int x = 0;
+      if (idx >= 0) {
+        const int code = __ldcg(hist + idx);
+        if ((code >> 1) == mb) x = (code & 1) ? -1 : 1;
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      const int c = carry + x;
+      if (idx >= 0) __stcg(memo + idx, __ldcg(memo + idx) + abs(c + md) - abs(c));
+      carry = __shfl_sync(FULL, c, 31);
+    }
+    if (lane == 0) __stcg(memo + hs.steps, 1);
+  }
+  __threadfence();
+  __syncwarp();
+  return active;
+}
+
 // Whole warp, after the last item of leaf li's step (do_step) or for its
 // first step: lane 0 runs the step (hill_step), then the warp screens the
 // next neighbourhood and enqueues the survivors. A neighbourhood with no
 // survivor cannot improve, so the next step runs at once (and stops).
-__device__ void advance_leaf(const Bufs& b, const AsyncQ& q, int li, int cls, int lane, bool do_step) {
+__device__ void advance_leaf(const Bufs& b, const AsyncQ& q, int li, int lane, bool do_step) {
   const Leaf lf = b.leaves[li];
+  int moved = -1;  // boundary of the last move (screen rows to refresh), -1: all
   for (;;) {
     if (do_step) {
       int active = 0;
-      if (lane == 0) {
-        HillState hs = b.hs[li];
-        int delta[HP_MAX_STAGES];
-        unsigned char old[2 * HP_MAX_STAGES];
-        int tmp[HP_MAX_STAGES];
-        for (int i = 0; i < lf.P; ++i) delta[i] = 0;
-        const int seq = hs.steps;
-        hill_step(c_consts, lf, b.lg + lf.lg_off, b.layouts + lf.layout_off, b.cur + lf.split_off,
-                  b.uni + lf.split_off, b.prop + lf.split_off, b.best + lf.split_off,
-                  b.hist + b.hist_off[li], hs, b.nb + b.nb_off[li], delta, old, tmp);
-        b.hs[li] = hs;
-        if (b.log.vals) {  // simulated, non-memo neighbours in visit order (planner.cpp:472-476)
+      if (b.log.vals == nullptr) {
+        active = hill_step_warp(b, li, lf, lane, moved);
+        if (lane == 0) {
+          if (b.trace) {
+            const int st = b.hs[li].steps;
+            trace_event(b, 0, li, lf, st > 0 ? (unsigned)b.hist[b.hist_off[li] + st - 1] : 0xfff);
+          }
+          if (!active) {
+            __threadfence();
+            atomicSub(q.active, 1);
+          }
+        }
+        if (!active) return;
+      } else {
+        if (lane == 0) {
+          HillState hs = b.hs[li];
+          int delta[HP_MAX_STAGES];
+          unsigned char old[2 * HP_MAX_STAGES];
+          int tmp[HP_MAX_STAGES];
+          for (int i = 0; i < lf.P; ++i) delta[i] = 0;
+          const int seq = hs.steps;
+          hill_step(c_consts, lf, b.lg + lf.lg_off, b.layouts + lf.layout_off, b.cur + lf.split_off,
+                    b.uni + lf.split_off, b.prop + lf.split_off, b.best + lf.split_off,
+                    b.hist + b.hist_off[li], hs, b.nb + b.nb_off[li], delta, old, tmp);
+          b.hs[li] = hs;
+          // simulated, non-memo neighbours in visit order (planner.cpp:472-476)
           const double* nbt = b.nb + b.nb_off[li];
           const int nslots = 2 * (lf.P - 1);
           int n = 0;
@@ -694,47 +1290,40 @@ __device__ void advance_leaf(const Bufs& b, const AsyncQ& q, int li, int cls, in
           if (off >= 0)
             for (int k = 0; k < nslots; ++k)
               if (!old[k] && nbt[k] >= 0) b.log.vals[off++] = nbt[k];
-        }
-        if (b.trace) {
-          unsigned long long now;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-          unsigned long long k = atomicAdd(b.trace, 1ULL);
-          if (k < (1ULL << 22)) {
-            b.trace[1 + 2 * k] = now;
-            const unsigned long long mv = hs.steps > 0 ? (unsigned)b.hist[b.hist_off[li] + hs.steps - 1] : 0xfff;
-            b.trace[2 + 2 * k] = ((unsigned long long)cls << 56) | ((unsigned long long)(lf.P & 0xff) << 48) |
-                                 ((unsigned long long)(lf.M & 0xffff) << 32) | ((mv & 0xfff) << 20) |
-                                 (unsigned)(li & 0xfffff);
+          if (b.trace) trace_event(b, 0, li, lf, hs.steps > 0 ? (unsigned)b.hist[b.hist_off[li] + hs.steps - 1] : 0xfff);
+          active = hs.active;
+          if (!active) {
+            __threadfence();
+            atomicSub(q.active, 1);
           }
         }
-        active = hs.active;
-        if (!active) {
-          __threadfence();
-          atomicSub(q.active, 1);
-        }
+        active = __shfl_sync(0xffffffffu, active, 0);
+        if (!active) return;
+        __syncwarp();
       }
-      active = __shfl_sync(0xffffffffu, active, 0);
-      if (!active) return;
-      __syncwarp();
     }
     do_step = true;
-    const int n = screen_neighbours(b, li, lf, lane);
+    const int n = screen_neighbours(b, li, lf, lane, moved);
+    if (b.trace && b.trace_items && lane == 0) trace_event(b, 3, li, lf, n);
     if (n > 0) {
-      if (lane == 0) push_items(b, q, li, cls, b.hs[li].steps >= kHiSteps ? 0 : 1, n);
+      const long long lv = (long long)__ldcg(&b.hs[li].steps) * (2 * (lf.M + lf.P - 1));
+      const bool hi = (q.crit && q.crit[li]) || lv >= q.hi_levels;
+      push_items(b, q, li, lf, hi ? 0 : 1, n, lane);
+      if (b.trace && b.trace_items && lane == 0) trace_event(b, 4, li, lf, 0);
       return;
     }
   }
 }
 
-// Enqueue the first step of every climbing leaf of class `cls` (a warp per leaf).
-__global__ void k_async_seed(Bufs b, AsyncQ q, const int* ids, int n, int cls) {
+// Enqueue the first step of every climbing leaf (a warp per leaf).
+__global__ void k_async_seed(Bufs b, AsyncQ q, const int* ids, int n) {
   const int lane = threadIdx.x & 31;
   const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (k >= n) return;
   const int li = ids[k];
   if (!b.hs[li].active) return;
   if (lane == 0) atomicAdd(q.active, 1);
-  advance_leaf(b, q, li, cls, lane, false);
+  advance_leaf(b, q, li, lane, false);
 }
 
 __device__ __forceinline__ bool try_slot(const AsyncQ& q, int lv, long long& ticket, Work& w) {
@@ -747,20 +1336,17 @@ __device__ __forceinline__ bool try_slot(const AsyncQ& q, int lv, long long& tic
   w.kind = __ldcg(&sl->kind);
   w.first = __ldcg(&sl->first);
   w.n = __ldcg(&sl->n);
+  w.out = __ldcg(&sl->out);
   ticket = -1;
   return true;
 }
 
 // Lane 0: next item for this warp (see AsyncQ). Tickets are claimed only
-// when the ring shows unclaimed items, so an idle warp holds none and may
-// retire: in the tail of a class (few leaves left), surplus idle warps exit
-// and free their SM for the next class's kernel, launched concurrently on
-// another stream. At least 64 warps per climbing leaf stay resident.
-// Returns false when the warp should exit.
+// when the ring shows unclaimed items, so an idle warp holds none.
+// Returns false when the warp should exit (no leaf climbing, or abort).
 __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[2]) {
   unsigned ns = 32;
   const long long t0 = clock64();
-  int idle = 0;
   for (;;) {
 #pragma unroll
     for (int lv = 0; lv < 2; ++lv) {
@@ -771,58 +1357,64 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[2]) {
     }
     const int act = *(volatile int*)q.active;
     if (act == 0 || *(volatile int*)q.abort) return false;
-    if (tk[0] < 0 && tk[1] < 0 && ++idle > 8 && act * 64 < *(volatile int*)q.live) {
-      if (atomicSub(q.live, 1) > act * 64) return false;
-      atomicAdd(q.live, 1);
-    }
     // watchdog: ~30 s without work while leaves are active means a bug
     if (clock64() - t0 > (1LL << 36)) {
       atomicExch(q.abort, 1);
       return false;
     }
     __nanosleep(ns);
-    if (ns < 1024) ns <<= 1;
+    if (ns < 256) ns <<= 1;
   }
 }
 
-// Resident blocks of 256 threads per SM the hill-climb kernels are compiled
-// for (register cap 65536 / (256 * n)); more warps hide the FP64 latency of
-// the level chain. HP_MINB_K<K> overrides at build time (tuning).
-#ifndef HP_MINB_2
-#define HP_MINB_2 3
+// Resident 256-thread blocks per SM the hill-climb kernel is compiled for
+// (register cap 65536 / (256 * n)). Fewer resident warps shorten each
+// warp's level latency (the long climbs are a chain of simulations whose
+// latency, not throughput, bounds the search); HP_ALL_MINB overrides at
+// build time (tuning).
+#ifndef HP_ALL_MINB
+#define HP_ALL_MINB 1
 #endif
-#ifndef HP_MINB_4
-#define HP_MINB_4 2
-#endif
-#ifndef HP_MINB_6
-#define HP_MINB_6 2
-#endif
-#ifndef HP_MINB_8
-#define HP_MINB_8 1
-#endif
-template <int K, bool FAST>
-constexpr int async_min_blocks() {
-  return !FAST ? 1 : (K == 2 ? HP_MINB_2 : K == 4 ? HP_MINB_4 : K == 6 ? HP_MINB_6 : HP_MINB_8);
-}
 
 template <int K, bool FAST>
-__global__ void __launch_bounds__(256, async_min_blocks<K, FAST>()) k_hill_async(Bufs b, AsyncQ q, int cls) {
+__device__ __noinline__ void eval_item_call(const Bufs& b, const Work& w, int lane) {
+  eval_item<K, FAST>(b, w, lane);
+}
+
+__global__ void __launch_bounds__(256, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ q) {
   const int lane = threadIdx.x & 31;
   long long tk[2] = {-1, -1};
   for (;;) {
-    int quit = 0;
+    int quit = 0, cls = 0;
     Work w{};
-    if (lane == 0) quit = pop_item(q, w, tk) ? 0 : 1;
+    if (lane == 0) {
+      quit = pop_item(q, w, tk) ? 0 : 1;
+      if (!quit) cls = w.out > 0 ? w.out - 1 : leaf_class(b.leaves[w.leaf]);
+    }
     quit = __shfl_sync(0xffffffffu, quit, 0);
     if (quit) return;
+    cls = __shfl_sync(0xffffffffu, cls, 0);
     w.leaf = __shfl_sync(0xffffffffu, w.leaf, 0);
     w.kind = __shfl_sync(0xffffffffu, w.kind, 0);
     w.first = __shfl_sync(0xffffffffu, w.first, 0);
     w.n = __shfl_sync(0xffffffffu, w.n, 0);
     w.out = 0;
     w.ids = w.kind == 1 ? b.nb_ids + b.nb_off[w.leaf] : nullptr;
-    eval_item<K, FAST>(b, w, lane);
+    const bool tr_item = b.trace && b.trace_items &&
+                         ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % b.trace_items == 0;
+    if (tr_item && lane == 0) trace_event(b, 1, w.leaf, b.leaves[w.leaf], w.first);
+    switch (cls) {
+      case 0: eval_item_call<2, true>(b, w, lane); break;
+      case 1: eval_item_call<4, true>(b, w, lane); break;
+      case 2: eval_item_call<6, true>(b, w, lane); break;
+      case 3: eval_item_call<8, true>(b, w, lane); break;
+      case 4: eval_item_call<1, false>(b, w, lane); break;
+      case 5: eval_item_call<2, false>(b, w, lane); break;
+      case 6: eval_item_call<3, false>(b, w, lane); break;
+      default: eval_item_call<8, false>(b, w, lane); break;
+    }
     __syncwarp();
+    if (tr_item && lane == 0) trace_event(b, 2, w.leaf, b.leaves[w.leaf], w.first);
     int last = 0;
     if (lane == 0) {
       __threadfence();
@@ -830,7 +1422,7 @@ __global__ void __launch_bounds__(256, async_min_blocks<K, FAST>()) k_hill_async
       if (last) __threadfence();
     }
     last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) advance_leaf(b, q, w.leaf, cls, lane, true);
+    if (last) advance_leaf(b, q, w.leaf, lane, true);
     __syncwarp();
   }
 }
@@ -1350,42 +1942,13 @@ static void launch_eval(int cls, const hpk::Bufs& b, const Work* items, const in
   }
 }
 
-template <int K, bool FAST>
-static int async_grid(int sm_count) {
+static int async_grid(int sm_count, int threads) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hpk::k_hill_async<K, FAST>, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hpk::k_hill_async, threads, 0);
+  if (const char* e = std::getenv("HP_ASYNC_BLOCKS")) per_sm = std::min(per_sm, std::atoi(e));  // tuning
   return sm_count * (per_sm > 0 ? per_sm : 1);
 }
 
-static int async_grid_of(int cls, int sm_count) {
-  switch (cls) {
-    case 0: return async_grid<2, true>(sm_count);
-    case 1: return async_grid<4, true>(sm_count);
-    case 2: return async_grid<6, true>(sm_count);
-    case 3: return async_grid<8, true>(sm_count);
-    case 4: return async_grid<1, false>(sm_count);
-    case 5: return async_grid<2, false>(sm_count);
-    case 6: return async_grid<3, false>(sm_count);
-    default: return async_grid<8, false>(sm_count);
-  }
-}
-
-static void launch_async(int cls, const hpk::Bufs& b, const hpk::AsyncQ& q, int grid,
-                         cudaStream_t st) {
-  switch (cls) {
-    case 0: hpk::k_hill_async<2, true><<<grid, 256, 0, st>>>(b, q, cls); break;
-    case 1: hpk::k_hill_async<4, true><<<grid, 256, 0, st>>>(b, q, cls); break;
-    case 2: hpk::k_hill_async<6, true><<<grid, 256, 0, st>>>(b, q, cls); break;
-    case 3: hpk::k_hill_async<8, true><<<grid, 256, 0, st>>>(b, q, cls); break;
-    case 4: hpk::k_hill_async<1, false><<<grid, 256, 0, st>>>(b, q, cls); break;
-    case 5: hpk::k_hill_async<2, false><<<grid, 256, 0, st>>>(b, q, cls); break;
-    case 6: hpk::k_hill_async<3, false><<<grid, 256, 0, st>>>(b, q, cls); break;
-    default: hpk::k_hill_async<8, false><<<grid, 256, 0, st>>>(b, q, cls); break;
-  }
-}
-
-// Split-independent tables of `my_leaves` (host, exact reference order),
-// uploaded with the per-leaf device state buffers.
 static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vector<int>& my_leaves,
                                 hpk::Bufs& b, std::vector<Leaf>& leaves, std::vector<int>& hill_ids,
                                 std::vector<int>& exh_ids) {
@@ -1451,6 +2014,8 @@ static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vect
   if (!(s = scratch(a, "nb", nb_total, &b.nb)).ok()) return s;
   if (!(s = scratch(a, "nb_ids", nb_total, &b.nb_ids)).ok()) return s;
   if (!(s = scratch(a, "lbs", split_total, &b.lbs)).ok()) return s;
+  if (!(s = scratch(a, "lbn", split_total, &b.lbn)).ok()) return s;
+  if (!(s = scratch(a, "memo_d", hist_total, &b.memo_d)).ok()) return s;
   if (!(s = scratch(a, "hs", nL, &b.hs)).ok()) return s;
   CK(cudaMemsetAsync(b.hs, 0, sizeof(HillState) * std::max(1, nL), st));
   return hph::Status{};
@@ -1586,103 +2151,95 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
                                                                    d_ctr + 16);
     out.launches++;
   }
-  std::vector<std::vector<int>> by_cls(hpk::NCLS);
-  std::vector<size_t> items_cls(hpk::NCLS, 0);
+  std::vector<int> climb;
+  size_t n_items = 0;
   for (int k : hill_ids) {
     if (leaves[k].mode != 0) continue;
+    climb.push_back(k);
     int cls = hpk::eval_class(leaves[k].P, leaves[k].M, leaves[k].sched == 0);
-    by_cls[cls].push_back(k);
     int cpw = hpk::class_cpw(cls, leaves[k].P);
-    items_cls[cls] += (2 * (leaves[k].P - 1) + cpw - 1) / cpw;
+    n_items += (2 * (leaves[k].P - 1) + cpw - 1) / cpw;
   }
   // Longest steps first: the seeding order is the initial queue order, so
   // the slowest leaves start early instead of forming the tail.
-  for (auto& v : by_cls)
-    std::stable_sort(v.begin(), v.end(), [&](int x, int y) {
-      return (double)leaves[x].M * leaves[x].P > (double)leaves[y].M * leaves[y].P;
-    });
-  size_t qcap = 1024;
-  for (int cls = 0; cls < hpk::NCLS; ++cls) qcap = std::max(qcap, items_cls[cls] + 1024);
+  std::stable_sort(climb.begin(), climb.end(), [&](int x, int y) {
+    return (double)leaves[x].M * leaves[x].P > (double)leaves[y].M * leaves[y].P;
+  });
   if (std::getenv("HP_DEBUG_TRACE")) {
     if (!(s = scratch(a, "trace", 1 + 2 * (1ULL << 22), &b.trace)).ok()) return s;
     CK(cudaMemsetAsync(b.trace, 0, sizeof(unsigned long long), st));
+    // HP_DEBUG_TRACE_ITEMS=n: item events of every n-th warp of the climb kernel
+    b.trace_items = std::getenv("HP_DEBUG_TRACE_ITEMS") ? std::max(1, std::atoi(std::getenv("HP_DEBUG_TRACE_ITEMS"))) : 0;
   }
-  // One queue per class; the class kernels run concurrently on side streams,
-  // largest class first, and retire idle warps in their tails (pop_item) so
-  // the next class fills the freed SMs.
-  int* d_pending;
-  if (!(s = scratch(a, "q_pending", nL, &d_pending)).ok()) return s;
+  // One queue and one persistent kernel for every evaluator class. A leaf
+  // has at most one step's items in the rings, so n_items bounds the fill.
+  hpk::AsyncQ q{};
   int* d_abort;
   if (!(s = scratch(a, "q_abort", 1, &d_abort)).ok()) return s;
   CK(cudaMemsetAsync(d_abort, 0, sizeof(int), st));
-  std::vector<int> order;
-  std::vector<double> cls_cost(hpk::NCLS, 0.0);
-  for (int cls = 0; cls < hpk::NCLS; ++cls) {
-    for (int k : by_cls[cls]) cls_cost[cls] += (double)leaves[k].M * leaves[k].P * leaves[k].P;
-    if (!by_cls[cls].empty()) order.push_back(cls);
-  }
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cls_cost[x] > cls_cost[y]; });
-  // class id lists go up on the main stream before the side streams fork
-  std::vector<int*> d_cls_ids(hpk::NCLS, nullptr);
-  for (int cls : order) {
-    std::string nm = "cls_ids" + std::to_string(cls);
-    if (!(s = upload(a, nm.c_str(), by_cls[cls], &d_cls_ids[cls])).ok()) return s;
-  }
-  cudaEvent_t ready = a.marker();
-  cudaEvent_t h0 = nullptr, h1 = nullptr;  // the concurrent class kernels as one timed region
-  if (a.time_evals && !order.empty()) {
-    a.event_pair(&h0, &h1);
-    CK(cudaEventRecord(h0, st));
-  }
-  CK(cudaEventRecord(ready, st));
-  std::vector<hpk::AsyncQ> qs(hpk::NCLS);
-  for (int cls : order) {
-    cudaStream_t ss = a.side(cls);
-    CK(cudaStreamWaitEvent(ss, ready, 0));
-    hpk::AsyncQ& q = qs[cls];
-    const size_t qcap = items_cls[cls] + 1024;
+  q.abort = d_abort;
+  if (!climb.empty()) {
+    if (!(s = scratch(a, "q_pending", nL, &q.pending)).ok()) return s;
+    int* d_climb;
+    if (!(s = upload(a, "climb_ids", climb, &d_climb)).ok()) return s;
+    const size_t qcap = n_items + 1024;
     for (int lv = 0; lv < 2; ++lv) {
-      std::string nm = "q_slots" + std::to_string(cls) + "_" + std::to_string(lv);
+      std::string nm = "q_slots" + std::to_string(lv);
       if (!(s = scratch(a, nm.c_str(), qcap, &q.slots[lv])).ok()) return s;
-      nm = "q_seq" + std::to_string(cls) + "_" + std::to_string(lv);
+      nm = "q_seq" + std::to_string(lv);
       if (!(s = scratch(a, nm.c_str(), qcap, &q.seq[lv])).ok()) return s;
-      CK(cudaMemsetAsync(q.seq[lv], 0, sizeof(unsigned long long) * qcap, ss));
+      CK(cudaMemsetAsync(q.seq[lv], 0, sizeof(unsigned long long) * qcap, st));
     }
     unsigned long long* d_q;
-    std::string nm = "q_ctr" + std::to_string(cls);
-    if (!(s = scratch(a, nm.c_str(), 8, &d_q)).ok()) return s;
+    if (!(s = scratch(a, "q_ctr", 8, &d_q)).ok()) return s;
+    CK(cudaMemsetAsync(d_q, 0, 8 * sizeof(unsigned long long), st));
     q.head[0] = d_q;
     q.head[1] = d_q + 1;
     q.tail[0] = d_q + 2;
     q.tail[1] = d_q + 3;
     q.active = reinterpret_cast<int*>(d_q + 4);
-    q.live = reinterpret_cast<int*>(d_q + 5);
-    q.abort = d_abort;
-    q.pending = d_pending;
     q.cap = qcap;
-    const int grid = async_grid_of(cls, a.sm_count);
-    unsigned long long init[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    reinterpret_cast<int*>(init + 5)[0] = grid * 8;  // warps of the launch
-    CK(cudaMemcpyAsync(d_q, init, sizeof init, cudaMemcpyHostToDevice, ss));
-    int n = static_cast<int>(by_cls[cls].size());
-    hpk::k_async_seed<<<(n * 32 + T - 1) / T, T, 0, ss>>>(b, q, d_cls_ids[cls], n, cls);
-    launch_async(cls, b, q, grid, ss);
+    q.hi_levels = 1LL << 20;
+    if (const char* e = std::getenv("HP_HI_LEVELS")) q.hi_levels = std::atoll(e);  // tuning
+    int threads = 256;
+    if (const char* e = std::getenv("HP_ASYNC_THREADS")) threads = std::atoi(e);  // tuning
+    const int grid = async_grid(a.sm_count, threads);
+    q.lat = std::getenv("HP_NO_LAT") ? 0 : 1;  // tuning
+    // critical leaves: longest expected climbs (P^2 M) while their neighbour
+    // items (~P-1 per step after the screen, one per warp at K = 4) fit the
+    // resident warps
+    {
+      long long budget = (long long)grid * (threads / 32);
+      if (const char* e = std::getenv("HP_CRIT_WARPS")) budget = std::atoll(e);  // tuning
+      std::vector<int> byest(climb);
+      std::stable_sort(byest.begin(), byest.end(), [&](int x, int y) {
+        return (double)leaves[x].P * leaves[x].P * leaves[x].M > (double)leaves[y].P * leaves[y].P * leaves[y].M;
+      });
+      std::vector<unsigned char> crit(nL, 0);
+      long long used = 0;
+      for (int k : byest) {
+        if (used + leaves[k].P - 1 > budget) break;
+        used += leaves[k].P - 1;
+        crit[k] = 1;
+      }
+      unsigned char* d_crit;
+      if (!(s = upload(a, "crit", crit, &d_crit)).ok()) return s;
+      q.crit = d_crit;
+    }
+    cudaEvent_t h0 = nullptr, h1 = nullptr;
+    if (a.time_evals) {
+      a.event_pair(&h0, &h1);
+      CK(cudaEventRecord(h0, st));
+    }
+    const int n = static_cast<int>(climb.size());
+    hpk::Bufs bh = b;
+    bh.nb_rows = b.log.vals == nullptr ? 1 : 0;  // the screen runs unless the log is recorded
+    hpk::k_async_seed<<<(n * 32 + T - 1) / T, T, 0, st>>>(bh, q, d_climb, n);
+    hpk::k_hill_async<<<grid, threads, 0, st>>>(bh, q);
+    if (h1) CK(cudaEventRecord(h1, st));
     out.launches += 2;
     out.eval_launches++;
   }
-  for (int cls : order) {
-    cudaEvent_t done = a.marker();
-    CK(cudaEventRecord(done, a.side(cls)));
-    CK(cudaStreamWaitEvent(st, done, 0));
-  }
-  if (h1) CK(cudaEventRecord(h1, st));
-  // the pinned init blocks above must outlive their copies
-  CK(cudaStreamSynchronize(st));
-  if (std::getenv("HP_DEBUG_TIMING") && a.time_evals) {
-    std::fprintf(stderr, "[hp] classes launched concurrently: %zu\n", order.size());
-  }
-  hpk::AsyncQ q = order.empty() ? hpk::AsyncQ{} : qs[order[0]];
-  q.abort = d_abort;
   out.hill_iterations = 0;
   if (b.trace) {
     CK(cudaStreamSynchronize(st));
@@ -1696,7 +2253,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
       std::fclose(fp);
     }
   }
-  if (!by_cls.empty()) {
+  if (!climb.empty()) {
     int abort_flag = 0;
     CK(cudaMemcpyAsync(&abort_flag, q.abort, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

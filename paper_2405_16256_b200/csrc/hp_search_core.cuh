@@ -318,6 +318,59 @@ HPD double nb_screen(const Consts& c, const Leaf& lf, const LeafGroup* lg, const
   return lb > cur_t * (1.0 + kScreenMargin) ? T_SKIP : 0.0;
 }
 
+// Durations of stage i of the current split at counts cur-1 ([0]) and
+// cur+1 ([1]), the only counts a neighbour gives a stage, with their status:
+// 0 count < 1 (planner.cpp:478), 1 memory-pruned, 2 feasible. Lets the
+// screen (nb_screen_pre) and the neighbour evaluation skip stage_setup.
+struct StageNb {
+  double f[2], b[2], dps[2];
+  int st[2];
+};
+
+HPD void lb_stage_nb(const Consts& c, const Leaf& lf, const LeafGroup* lg, const uint8_t* slots,
+                     const double* hop, int i, int count, StageNb& n) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int cc = count + (k ? 1 : -1);
+    StageDur d;
+    d.f = d.b = d.dps = 0.0;
+    int st = 0;
+    if (cc >= 1) st = stage_setup(c, lf, lg, slots, hop, i, cc, d) ? 2 : 1;
+    n.f[k] = d.f;
+    n.b[k] = d.b;
+    n.dps[k] = d.dps;
+    n.st[k] = st;
+  }
+}
+
+// nb_screen with the changed stages' durations taken from StageNb rows
+// (same value for every slot).
+HPD double nb_screen_pre(const Leaf& lf, const StageLB* s, const StageNb* nbs, int q, double cur_t) {
+  const int P = lf.P;
+  const int bb = q >> 1;
+  const int k0 = (q & 1) ? 0 : 1;  // +1 moves a layer into stage bb, out of bb+1
+  const int k1 = 1 - k0;
+  const int st0 = HP_LDX(&nbs[bb].st[k0]), st1 = HP_LDX(&nbs[bb + 1].st[k1]);
+  if (st0 == 0 || st1 == 0) return T_INVALID;
+  if (st0 == 1 || st1 == 1) return T_MEMORY;
+  const double f0 = HP_LDX(&nbs[bb].f[k0]), b0 = HP_LDX(&nbs[bb].b[k0]), p0 = HP_LDX(&nbs[bb].dps[k0]);
+  const double f1 = HP_LDX(&nbs[bb + 1].f[k1]), b1 = HP_LDX(&nbs[bb + 1].b[k1]);
+  const double p1 = HP_LDX(&nbs[bb + 1].dps[k1]);
+  const double M = (double)lf.M;
+  const double dps0 = bb == 0 ? p0 : HP_LDX(&s[0].dps);
+  double lb = dmax(HP_LDX(&s[bb].PX) + dps0, HP_LDX(&s[bb].PY));
+  const double A0 = HP_LDX(&s[bb].A), B0 = HP_LDX(&s[bb].Bt), sf0 = HP_LDX(&s[bb].sf);
+  lb = dmax(lb, A0 + M * (f0 + b0) + dmax(B0 + dps0, p0));
+  const double A1 = A0 + f0 + sf0, B1 = B0 + sf0 + b0;
+  lb = dmax(lb, A1 + M * (f1 + b1) + dmax(B1 + dps0, p1));
+  if (bb + 2 < P) {
+    const double dA = (f0 - HP_LDX(&s[bb].f)) + (f1 - HP_LDX(&s[bb + 1].f));
+    const double dB = (b0 - HP_LDX(&s[bb].b)) + (b1 - HP_LDX(&s[bb + 1].b));
+    lb = dmax(lb, dmax(HP_LDX(&s[bb + 2].SX) + dA + dB + dps0, HP_LDX(&s[bb + 2].SY) + dA));
+  }
+  return lb > cur_t * (1.0 + kScreenMargin) ? T_SKIP : 0.0;
+}
+
 // ------------------------------------------------------------ hill climb
 
 // Per-leaf state of the steepest-descent search (planner.cpp:461-489) plus

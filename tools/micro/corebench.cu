@@ -59,11 +59,15 @@ void run(int blocks_per_sm, int threads) {
     if (rep) best = ms < best ? ms : best;
   }
   double ops = (double)sms * blocks_per_sm * threads * levels * K * 4;
-  printf("core K=%d warps/SM=%2d : %6.2f T alg-ops/s (%.1f upd/clk/SM)\n", K, blocks_per_sm * threads / 32,
-         ops / best / 1e9, ops / 4 / best * 1e3 / sms / 1.965e9);
+  printf("core K=%d warps/SM=%2d : %6.2f T alg-ops/s (%.1f upd/clk/SM) %.1f cyc/level/warp\n", K,
+         blocks_per_sm * threads / 32, ops / best / 1e9, ops / 4 / best * 1e3 / sms / 1.965e9,
+         best * 1e-3 * 1.965e9 / levels);
 }
 
 int main() {
+  // latency: one warp per SM, then one per SM sub-partition
+  run<2>(1, 32); run<4>(1, 32); run<6>(1, 32); run<8>(1, 32);
+  run<2>(1, 128); run<4>(1, 128); run<6>(1, 128); run<8>(1, 128);
   for (int w : {2, 4, 8}) { run<2>(w, 128); run<4>(w, 128); run<6>(w, 128); run<8>(w, 128); }
   return 0;
 }

@@ -13,4 +13,5 @@ else:
 for _ in range(reps):
     t0 = time.time(); o = planner.search(cfg); t1 = time.time()
     print(json.dumps({"cfg": name, "wall_s": t1 - t0, "dev_ms": o.device_ms, "sim": o.candidates_simulated,
-                      "pruned": o.candidates_pruned, "t": o.iteration_time_s, "launches": o.gpu_launches}), flush=True)
+                      "pruned": o.candidates_pruned, "t": o.iteration_time_s, "launches": o.gpu_launches,
+                      "ops": o.raw.eval_fp64_ops}), flush=True)
