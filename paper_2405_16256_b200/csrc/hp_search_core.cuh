@@ -343,9 +343,10 @@ HPD void lb_stage_nb(const Consts& c, const Leaf& lf, const LeafGroup* lg, const
   }
 }
 
-// nb_screen with the changed stages' durations taken from StageNb rows
-// (same value for every slot).
-HPD double nb_screen_pre(const Leaf& lf, const StageLB* s, const StageNb* nbs, int q, double cur_t) {
+// nb_screen's path lower bound of neighbour slot q with the changed stages'
+// durations taken from StageNb rows (same value for every slot). Returns
+// T_INVALID / T_MEMORY for an infeasible neighbour, else the bound (>= 0).
+HPD double nb_lb_pre(const Leaf& lf, const StageLB* s, const StageNb* nbs, int q) {
   const int P = lf.P;
   const int bb = q >> 1;
   const int k0 = (q & 1) ? 0 : 1;  // +1 moves a layer into stage bb, out of bb+1
@@ -363,12 +364,23 @@ HPD double nb_screen_pre(const Leaf& lf, const StageLB* s, const StageNb* nbs, i
   lb = dmax(lb, A0 + M * (f0 + b0) + dmax(B0 + dps0, p0));
   const double A1 = A0 + f0 + sf0, B1 = B0 + sf0 + b0;
   lb = dmax(lb, A1 + M * (f1 + b1) + dmax(B1 + dps0, p1));
-  if (bb + 2 < P) {
-    const double dA = (f0 - HP_LDX(&s[bb].f)) + (f1 - HP_LDX(&s[bb + 1].f));
-    const double dB = (b0 - HP_LDX(&s[bb].b)) + (b1 - HP_LDX(&s[bb + 1].b));
-    lb = dmax(lb, dmax(HP_LDX(&s[bb + 2].SX) + dA + dB + dps0, HP_LDX(&s[bb + 2].SY) + dA));
-  }
+  const double fbb = HP_LDX(&s[bb].f), fb1 = HP_LDX(&s[bb + 1].f);
+  const double bbb = HP_LDX(&s[bb].b), bb1 = HP_LDX(&s[bb + 1].b);
+  const double dA = (f0 - fbb) + (f1 - fb1);
+  const double dB = (b0 - bbb) + (b1 - bb1);
+  if (bb + 2 < P) lb = dmax(lb, dmax(HP_LDX(&s[bb + 2].SX) + dA + dB + dps0, HP_LDX(&s[bb + 2].SY) + dA));
+  return dmax(lb, 0.0);
+}
+
+// Screen decision from nb_lb_pre: T_INVALID / T_MEMORY, T_SKIP when the
+// bound is above cur_t (with the margin), else 0.0 (simulate).
+HPD double screen_of(double lb, double cur_t) {
+  if (lb < 0) return lb;
   return lb > cur_t * (1.0 + kScreenMargin) ? T_SKIP : 0.0;
+}
+
+HPD double nb_screen_pre(const Leaf& lf, const StageLB* s, const StageNb* nbs, int q, double cur_t) {
+  return screen_of(nb_lb_pre(lf, s, nbs, q), cur_t);
 }
 
 // ------------------------------------------------------------ hill climb

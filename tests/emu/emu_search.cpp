@@ -1,3 +1,4 @@
+#include <algorithm>
 // TEST HARNESS ONLY — CPU emulation of the GPU search decomposition.
 //
 // Drives the exact per-candidate / per-leaf functions the sm_100a kernels run
@@ -17,6 +18,8 @@ using namespace hpc;
 namespace {
 
 long long g_screened = 0, g_neighbours = 0;  // nb_screen statistics (T_SKIP / all)
+long long g_screen_mismatch = 0;              // nb_screen_pre != nb_screen (must stay 0)
+long long g_bound_viol = 0;                   // nb_lb_pre above a simulated time (must stay 0)
 
 struct LeafDev {
   Leaf lf;
@@ -100,12 +103,22 @@ extern "C" int emu_search_shard(const hp_problem* in, int shard, int count, hp_r
       hill_init(c, L.lf, L.lg.data(), L.slots, uni.data(), prop.data(), tu, tp, cur.data(), bs.data(),
                 hs, L.lf.mode == 2);
       std::vector<StageLB> slb(P);
+      std::vector<StageNb> snb(P);
+      std::vector<double> lbv(2 * P);
       while (hs.active) {
-        // the GPU's neighbour screen (nb_screen): only survivors are simulated
-        for (int i = 0; i < P; ++i) lb_stage(c, L.lf, L.lg.data(), L.slots, L.hop, i, cur[i], slb[i]);
+        // the GPU's neighbour screen (nb_screen_pre over StageLB / StageNb
+        // rows): only survivors are simulated
+        for (int i = 0; i < P; ++i) {
+          lb_stage(c, L.lf, L.lg.data(), L.slots, L.hop, i, cur[i], slb[i]);
+          lb_stage_nb(c, L.lf, L.lg.data(), L.slots, L.hop, i, cur[i], snb[i]);
+        }
         lb_scan(L.lf, slb.data());
         for (int q = 0; q < 2 * (P - 1); ++q) {
-          double scr = nb_screen(c, L.lf, L.lg.data(), L.slots, L.hop, cur.data(), slb.data(), q, hs.cur_time);
+          const double lbq = nb_lb_pre(L.lf, slb.data(), snb.data(), q);
+          lbv[q] = lbq;
+          double scr = screen_of(lbq, hs.cur_time);
+          double ref = nb_screen(c, L.lf, L.lg.data(), L.slots, L.hop, cur.data(), slb.data(), q, hs.cur_time);
+          if (!(scr == ref)) g_screen_mismatch++;
           g_neighbours++;
           if (scr == T_SKIP) g_screened++;
           if (scr != 0.0) {
@@ -116,6 +129,8 @@ extern "C" int emu_search_shard(const hp_problem* in, int shard, int count, hp_r
           tmp = cur;
           tmp[b] += d; tmp[b + 1] -= d;
           nb[q] = eval(c, L, tmp.data());
+          // the bound must hold (up to the screen's rounding margin)
+          if (nb[q] >= 0 && lbq > nb[q] * (1.0 + 1e-9)) g_bound_viol++;
         }
         hill_step(c, L.lf, L.lg.data(), L.slots, cur.data(), uni.data(), prop.data(), bs.data(),
                   hist.data(), hs, nb.data(), delta.data(), old.data(), tmp.data());
@@ -145,6 +160,9 @@ extern "C" void emu_screen_stats(long long* screened, long long* neighbours, int
   *neighbours = g_neighbours;
   if (reset) g_screened = g_neighbours = 0;
 }
+
+extern "C" long long emu_screen_mismatches() { return g_screen_mismatch; }
+extern "C" long long emu_bound_violations() { return g_bound_viol; }
 
 // Explicit-plan evaluation through the same per-stage setup + serial
 // level-synchronous simulation (mode 3 pseudo-leaf, like hp_evaluate_plans).

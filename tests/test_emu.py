@@ -43,6 +43,13 @@ def test_emu_matches_reference_full_mode(search_cases, emu):
     assert n >= 60
     emu.emu_screen_stats(C.byref(sk), C.byref(nn), 1)
     assert sk.value > 0.3 * nn.value, (sk.value, nn.value)
+    # the screen from precomputed count -1 / +1 stage rows (nb_screen_pre, the
+    # GPU's) decides exactly like the per-neighbour stage_setup one
+    emu.emu_screen_mismatches.restype = C.c_longlong
+    assert emu.emu_screen_mismatches() == 0
+    # and the bound never exceeds a simulated time
+    emu.emu_bound_violations.restype = C.c_longlong
+    assert emu.emu_bound_violations() == 0
 
 
 def test_emu_shards_partition_the_leaves(search_cases, emu):

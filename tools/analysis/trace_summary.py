@@ -10,10 +10,11 @@ import sys
 import numpy as np
 
 raw = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 2)
+raw = raw[((raw[:, 1] >> np.uint64(59)) & np.uint64(0xf)) == 0]  # step events only
 ns = raw[:, 0].astype(np.int64)
 pk = raw[:, 1]
 t = (ns - ns.min()) / 1e6  # ms
-cls = (pk >> np.uint64(56)).astype(int)
+cls = ((pk >> np.uint64(56)) & np.uint64(0x7)).astype(int)
 P = ((pk >> np.uint64(48)) & np.uint64(0xff)).astype(int)
 M = ((pk >> np.uint64(32)) & np.uint64(0xffff)).astype(int)
 leaf = (pk & np.uint64(0xfffff)).astype(int)
