@@ -367,6 +367,19 @@ __device__ __forceinline__ void eval_item_generic(const Bufs& b, const Work& w, 
 // the whole warp follows one instruction stream (no divergence) and only the
 // warm-up/cool-down windows are predicated. Segments are packed at exact
 // width W = ceil(P/K) (floor(32/W) candidates per warp).
+// HP_DEBUG_TRACE_ITEMS cycle records from inside the evaluator (ev 5: core
+// loop cycles, ev 6: whole item cycles; the timestamp slot holds the count,
+// aux = 1 when the core ran without channel maxima).
+__device__ void trace_cycles(const Bufs& b, int ev, int li, int P, int M, unsigned aux, long long cyc) {
+  unsigned long long k = atomicAdd(b.trace, 1ULL);
+  if (k < (1ULL << 22)) {
+    b.trace[1 + 2 * k] = (unsigned long long)cyc;
+    b.trace[2 + 2 * k] = ((unsigned long long)ev << 59) | ((unsigned long long)(P & 0xff) << 48) |
+                         ((unsigned long long)(M & 0xffff) << 32) | ((unsigned long long)(aux & 0xfff) << 20) |
+                         (unsigned)(li & 0xfffff);
+  }
+}
+
 // Core-loop level pairs between early-abort checks of a screened neighbour.
 constexpr int kAbortPairs = 64;
 
@@ -496,6 +509,11 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
                                                 : __builtin_huge_val();
   bool dead = false;
   int dead_t = 0;
+  const bool tr = b.trace && b.trace_items && lane == 0 &&
+                  ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % b.trace_items == 0;
+  const long long c_start = tr ? clock64() : 0;
+  long long c_core0 = 0, c_core1 = 0;
+  bool tr_noch = false;
   if (__any_sync(0xffffffffu, run)) {
     // ---- warm-up, levels 0..P-1: stage i runs F(i, t-i) once t >= i
     for (int t = 0; t < P; ++t) {
@@ -527,8 +545,14 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
       constexpr int PAR = decltype(par_tag)::value;
       constexpr bool PRED = decltype(pred_tag)::value;
       constexpr int MODE = decltype(mode_tag)::value;
-      const double lchf = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
-      const double rchb = __shfl_sync(0xffffffffu, chb[0], src_r);
+      // K is even: at odd levels the lane's first stage runs a backward and
+      // its last a forward, both fed by the lane's own neighbours, so only
+      // even levels exchange across lanes
+      double lchf = 0.0, rchb = 0.0;
+      if (PAR == 0) {
+        lchf = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
+        rchb = __shfl_sync(0xffffffffu, chb[0], src_r);
+      }
       const int u0 = t + sl * K;  // t + i - r
       const int v0 = t - sl * K;  // t - i + r
 #pragma unroll
@@ -617,6 +641,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
         }
       }
       bool noch = false;
+      if (tr) c_core0 = clock64();
       if (t + 1 <= core_hi) {
         level(I0{}, PF{}, M1{}, t);
         level(I1{}, PF{}, M1{}, t + 1);
@@ -675,8 +700,16 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
         level(I0{}, PF{}, M0{}, t);
         ++t;
       }
+      if (tr) {
+        c_core1 = clock64();
+        tr_noch = noch;
+      }
     }
     for (; t < T; ++t) pred_level(t);
+  }
+  if (tr) {
+    trace_cycles(b, 5, w.leaf, P, M, tr_noch ? 1 : 0, c_core1 - c_core0);
+    trace_cycles(b, 6, w.leaf, P, M, K, clock64() - c_start);
   }
   double v = 0.0;
 #pragma unroll
@@ -759,6 +792,7 @@ struct AsyncQ {
   long long hi_levels;          // priority threshold (see above)
   const unsigned char* crit;    // per leaf: critical (level 0 from the first step)
   int lat;                      // level-0 items use lat_class
+  int lead;                     // level 0 is served by warps 0-3 of each block only
 };
 
 __device__ __forceinline__ int leaf_class(const Leaf& lf) { return eval_class(lf.P, lf.M, lf.sched == 0); }
@@ -968,17 +1002,24 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
     lb_scan_warp(lf, sl, lane);
     __syncwarp();
   }
-  int n = 0;
-  for (int q0 = 0; q0 < nslots; q0 += 32) {
-    const int qq = q0 + lane;
-    bool surv = false;
+  // all of the lane's slots first (independent loads in flight together),
+  // then the survivor list in slot order
+  constexpr int NQ = (2 * HP_MAX_STAGES + 31) / 32;
+  unsigned sv = 0;
+#pragma unroll
+  for (int j = 0; j < NQ; ++j) {
+    const int qq = 32 * j + lane;
     if (qq < nslots) {
       const double scr = screen ? nb_screen_pre(lf, sl, sn, qq, cur_t) : 0.0;
-      if (scr == 0.0) surv = true;
+      if (scr == 0.0) sv |= 1u << j;
       else nbt[qq] = scr;
     }
+  }
+  int n = 0;
+  for (int j = 0; 32 * j < nslots; ++j) {
+    const bool surv = (sv >> j) & 1u;
     const unsigned m = __ballot_sync(0xffffffffu, surv);
-    if (surv) ids[n + __popc(m & ((1u << lane) - 1u))] = qq;
+    if (surv) ids[n + __popc(m & ((1u << lane) - 1u))] = 32 * j + lane;
     n += __popc(m);
   }
   __threadfence();
@@ -1012,9 +1053,17 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
   int* memo = b.memo_d + b.hist_off[li];
   unsigned oldm = 0;  // bit 2k + (dir < 0) for my boundary lane + 32k
   bool all_old = false;
-  for (int t0 = hs.steps - 1; t0 >= 0; t0 -= 32) {
-    const int idx = t0 - lane;
-    const int dv = idx >= 0 ? __ldcg(memo + idx) : 3;
+  for (int t1 = hs.steps - 1; t1 >= 0; t1 -= 128) {
+   int dvs[4];
+#pragma unroll
+   for (int u = 0; u < 4; ++u) {
+    const int idx = t1 - 32 * u - lane;
+    dvs[u] = idx >= 0 ? __ldcg(memo + idx) : 3;
+   }
+#pragma unroll
+   for (int u = 0; u < 4; ++u) {
+    const int t0 = t1 - 32 * u;
+    const int dv = dvs[u];
     unsigned fl = __ballot_sync(FULL, dv <= 2);
     while (fl) {
       const int j = __ffs(fl) - 1;
@@ -1041,6 +1090,7 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
       for (int k = 0; k < NK; ++k)
         if (dl[k] != 0) oldm |= 1u << (2 * k + (dl[k] > 0 ? 1 : 0));  // toward c_t
     }
+   }
   }
   // seeds at distance 1: prefix sums of cur - ref over each lane's chunk
   {
@@ -1223,21 +1273,32 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
     // D_k(k+1) = 1
     const int mb = mq >> 1, md = (mq & 1) ? -1 : 1;
     int carry = 0;
-    for (int t0 = hs.steps - 1; t0 >= 0; t0 -= 32) {
-      const int idx = t0 - lane;
-      int x = 0;
-      if (idx >= 0) {
-        const int code = __ldcg(hist + idx);
-        if ((code >> 1) == mb) x = (code & 1) ? -1 : 1;
+    for (int t1 = hs.steps - 1; t1 >= 0; t1 -= 128) {
+      int xs[4], ms[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = t1 - 32 * u - lane;
+        xs[u] = 0;
+        ms[u] = 0;
+        if (idx >= 0) {
+          const int code = __ldcg(hist + idx);
+          if ((code >> 1) == mb) xs[u] = (code & 1) ? -1 : 1;
+          ms[u] = __ldcg(memo + idx);
+        }
       }
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, x, o);
-        if (lane >= o) x += y;
+      for (int u = 0; u < 4; ++u) {
+        const int idx = t1 - 32 * u - lane;
+        int x = xs[u];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, x, o);
+          if (lane >= o) x += y;
+        }
+        const int c = carry + x;
+        if (idx >= 0) __stcg(memo + idx, ms[u] + abs(c + md) - abs(c));
+        carry = __shfl_sync(FULL, c, 31);
       }
-      const int c = carry + x;
-      if (idx >= 0) __stcg(memo + idx, __ldcg(memo + idx) + abs(c + md) - abs(c));
-      carry = __shfl_sync(FULL, c, 31);
     }
     if (lane == 0) __stcg(memo + hs.steps, 1);
   }
@@ -1344,12 +1405,13 @@ __device__ __forceinline__ bool try_slot(const AsyncQ& q, int lv, long long& tic
 // Lane 0: next item for this warp (see AsyncQ). Tickets are claimed only
 // when the ring shows unclaimed items, so an idle warp holds none.
 // Returns false when the warp should exit (no leaf climbing, or abort).
-__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[2]) {
+__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[2], int lv0) {
   unsigned ns = 32;
   const long long t0 = clock64();
   for (;;) {
 #pragma unroll
     for (int lv = 0; lv < 2; ++lv) {
+      if (lv < lv0) continue;
       if (tk[lv] < 0 &&
           *(volatile unsigned long long*)q.tail[lv] > *(volatile unsigned long long*)q.head[lv])
         tk[lv] = (long long)atomicAdd(q.head[lv], 1ULL);
@@ -1388,7 +1450,10 @@ __global__ void __launch_bounds__(256, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ 
     int quit = 0, cls = 0;
     Work w{};
     if (lane == 0) {
-      quit = pop_item(q, w, tk) ? 0 : 1;
+      // priority items go to the first warp of each SM sub-partition (warps
+      // 0-3 of the block), so two of them never share one: a climb step
+      // waits for its slowest item
+      quit = pop_item(q, w, tk, (threadIdx.x >> 5) < 4 || !q.lead ? 0 : 1) ? 0 : 1;
       if (!quit) cls = w.out > 0 ? w.out - 1 : leaf_class(b.leaves[w.leaf]);
     }
     quit = __shfl_sync(0xffffffffu, quit, 0);
@@ -2209,7 +2274,8 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     // items (~P-1 per step after the screen, one per warp at K = 4) fit the
     // resident warps
     {
-      long long budget = (long long)grid * (threads / 32);
+      q.lead = (threads == 256 && !std::getenv("HP_NO_LEAD")) ? 1 : 0;  // tuning
+      long long budget = (long long)grid * (q.lead ? 4 : threads / 32);
       if (const char* e = std::getenv("HP_CRIT_WARPS")) budget = std::atoll(e);  // tuning
       std::vector<int> byest(climb);
       std::stable_sort(byest.begin(), byest.end(), [&](int x, int y) {
