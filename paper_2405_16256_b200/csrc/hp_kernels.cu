@@ -181,11 +181,14 @@ __host__ __device__ inline int class_width(int cls, int P) {
 // climb kernel's 8 warps per SM (tools/micro/corebench: 6.4, 10.0, 11.5,
 // 11.2 T ops/s for K = 2..8 — more stages per lane is more independent FP64
 // work per warp, which at this occupancy hides the level's latency).
+#ifndef HP_FAST_KMAX
+#define HP_FAST_KMAX 8  // tuning: largest K chosen when a smaller one fits (K = 8 needs the most registers)
+#endif
 __host__ __device__ inline int fast_K(int P) {
   const double rate[4] = {6.4, 10.0, 11.5, 11.2};
   int bestK = 8;
   double bestU = -1.0;
-  for (int K = 2; K <= 8; K += 2) {
+  for (int K = 2; K <= HP_FAST_KMAX; K += 2) {
     int W = (P + K - 1) / K;
     if (W > 32) continue;
     double u = (double)P * (32 / W) / (32.0 * K) * rate[K / 2 - 1];
@@ -1450,10 +1453,12 @@ __global__ void __launch_bounds__(256, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ 
     int quit = 0, cls = 0;
     Work w{};
     if (lane == 0) {
-      // priority items go to the first warp of each SM sub-partition (warps
-      // 0-3 of the block), so two of them never share one: a climb step
-      // waits for its slowest item
-      quit = pop_item(q, w, tk, (threadIdx.x >> 5) < 4 || !q.lead ? 0 : 1) ? 0 : 1;
+      // priority items go to one warp per SM sub-partition (hardware warp
+      // slots 0-3), so two of them never share one: a climb step waits for
+      // its slowest item
+      unsigned slot;
+      asm volatile("mov.u32 %0, %%warpid;" : "=r"(slot));
+      quit = pop_item(q, w, tk, slot < 4 || !q.lead ? 0 : 1) ? 0 : 1;
       if (!quit) cls = w.out > 0 ? w.out - 1 : leaf_class(b.leaves[w.leaf]);
     }
     quit = __shfl_sync(0xffffffffu, quit, 0);
@@ -2274,8 +2279,8 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     // items (~P-1 per step after the screen, one per warp at K = 4) fit the
     // resident warps
     {
-      q.lead = (threads == 256 && !std::getenv("HP_NO_LEAD")) ? 1 : 0;  // tuning
-      long long budget = (long long)grid * (q.lead ? 4 : threads / 32);
+      q.lead = std::getenv("HP_NO_LEAD") ? 0 : 1;  // tuning
+      long long budget = q.lead ? (long long)a.sm_count * 4 : (long long)grid * (threads / 32);
       if (const char* e = std::getenv("HP_CRIT_WARPS")) budget = std::atoll(e);  // tuning
       std::vector<int> byest(climb);
       std::stable_sort(byest.begin(), byest.end(), [&](int x, int y) {
