@@ -544,24 +544,20 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
     // send waits for its channel (base_ok); 2: channel maxima dropped (see
     // the core loop below).
     bool base_ok = true;
+    // Cross-lane operands of the next even level (see `level`): the left
+    // neighbour's last forward channel and the right neighbour's first
+    // backward channel.
+    double xl = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
+    double xr = __shfl_sync(0xffffffffu, chb[0], src_r);
     auto level = [&](auto par_tag, auto pred_tag, auto mode_tag, int t) {
       constexpr int PAR = decltype(par_tag)::value;
       constexpr bool PRED = decltype(pred_tag)::value;
       constexpr int MODE = decltype(mode_tag)::value;
-      // K is even: at odd levels the lane's first stage runs a backward and
-      // its last a forward, both fed by the lane's own neighbours, so only
-      // even levels exchange across lanes
-      double lchf = 0.0, rchb = 0.0;
-      if (PAR == 0) {
-        lchf = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
-        rchb = __shfl_sync(0xffffffffu, chb[0], src_r);
-      }
       const int u0 = t + sl * K;  // t + i - r
       const int v0 = t - sl * K;  // t - i + r
-#pragma unroll
-      for (int r = 0; r < K; ++r) {
+      auto op = [&](int r) {
         if (((PAR - r) & 1) == 0) {
-          const double recv = r == 0 ? lchf : chf[r > 0 ? r - 1 : 0];
+          const double recv = r == 0 ? xl : chf[r > 0 ? r - 1 : 0];
           const double nfr = dmax(fr[r], recv) + f[r];
           if (MODE == 1) base_ok = base_ok && !(chf[r] > nfr);
           const double nch = (MODE == 2 ? nfr : dmax(nfr, chf[r])) + sf[r];
@@ -575,7 +571,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
             chf[r] = nch;
           }
         } else {
-          const double recv = r == K - 1 ? rchb : chb[r < K - 1 ? r + 1 : 0];
+          const double recv = r == K - 1 ? xr : chb[r < K - 1 ? r + 1 : 0];
           const double nfr = dmax(fr[r], recv) + bw[r];
           if (MODE == 1) base_ok = base_ok && !(chb[r] > nfr);
           const double nch = (MODE == 2 ? nfr : dmax(nfr, chb[r])) + (r == 0 ? sb0 : sf[r > 0 ? r - 1 : 0]);
@@ -589,6 +585,23 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
             chb[r] = nch;
           }
         }
+      };
+      // K is even: at odd levels a lane's first stage runs a backward and
+      // its last a forward, both fed by the lane's own stages, and they
+      // produce exactly what the neighbours need at the next (even) level.
+      // So odd levels compute those two stages first and send their channel
+      // ends right away — the exchange overlaps the interior stages — and
+      // even levels read them (xl, xr) without exchanging.
+      if (PAR == 1) {
+        op(0);
+        op(K - 1);
+        xl = __shfl_sync(0xffffffffu, chf[K - 1], src_l);
+        xr = __shfl_sync(0xffffffffu, chb[0], src_r);
+#pragma unroll
+        for (int r = 1; r < K - 1; ++r) op(r);
+      } else {
+#pragma unroll
+        for (int r = 0; r < K; ++r) op(r);
       }
     };
     using I0 = std::integral_constant<int, 0>;
@@ -1453,12 +1466,10 @@ __global__ void __launch_bounds__(256, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ 
     int quit = 0, cls = 0;
     Work w{};
     if (lane == 0) {
-      // priority items go to one warp per SM sub-partition (hardware warp
-      // slots 0-3), so two of them never share one: a climb step waits for
-      // its slowest item
-      unsigned slot;
-      asm volatile("mov.u32 %0, %%warpid;" : "=r"(slot));
-      quit = pop_item(q, w, tk, slot < 4 || !q.lead ? 0 : 1) ? 0 : 1;
+      // priority items go to one warp per SM sub-partition (warps 0-3 of
+      // the SM's one block), so two of them never share one: a climb step
+      // waits for its slowest item
+      quit = pop_item(q, w, tk, (threadIdx.x >> 5) < 4 || !q.lead ? 0 : 1) ? 0 : 1;
       if (!quit) cls = w.out > 0 ? w.out - 1 : leaf_class(b.leaves[w.leaf]);
     }
     quit = __shfl_sync(0xffffffffu, quit, 0);
@@ -2279,8 +2290,8 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     // items (~P-1 per step after the screen, one per warp at K = 4) fit the
     // resident warps
     {
-      q.lead = std::getenv("HP_NO_LEAD") ? 0 : 1;  // tuning
-      long long budget = q.lead ? (long long)a.sm_count * 4 : (long long)grid * (threads / 32);
+      q.lead = (threads >= 128 && !std::getenv("HP_NO_LEAD")) ? 1 : 0;  // tuning
+      long long budget = (long long)grid * (q.lead ? 4 : threads / 32);
       if (const char* e = std::getenv("HP_CRIT_WARPS")) budget = std::atoll(e);  // tuning
       std::vector<int> byest(climb);
       std::stable_sort(byest.begin(), byest.end(), [&](int x, int y) {
