@@ -617,6 +617,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
     };
     int t = P;
     for (; t < T && t < core_lo; ++t) pred_level(t);
+    bool cool_noch = false;  // cool-down without channel maxima (below)
     if (core_lo <= core_hi) {
       // core_lo is even: pairs (even, odd), then the final even level.
       // Channel maxima: in the core every stage alternates F and B, so
@@ -629,7 +630,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
       // core starts without waiting (MODE 1), the channel maxima are no-ops
       // and are dropped (MODE 2). The rounding slack is 4 ulps of an upper
       // bound on every node value: M * sum over stages of (f + b + sf + sb).
-      bool chok = true;
+      bool chok = true, chok2 = true;
       {
         double vs = 0.0;
 #pragma unroll
@@ -653,6 +654,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
             const double sbk = r == 0 ? sb0 : sf[r > 0 ? r - 1 : 0];
             const double fb = (f[r] + bw[r]) - slack;
             chok = chok && sf[r] < fb && sbk < fb;
+            chok2 = chok2 && sbk < bw[r] - slack;
           }
         }
       }
@@ -663,6 +665,11 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
         level(I1{}, PF{}, M1{}, t + 1);
         t += 2;
         noch = __all_sync(0xffffffffu, !run || (chok && base_ok));
+        // Cool-down: a stage keeps alternating until its last forward, then
+        // runs its trailing backwards two levels apart with nothing between,
+        // so B_end(j+1) >= B_end(j) + b: with sb < b (same rounding margin)
+        // the backward sends cannot wait either.
+        cool_noch = noch && __all_sync(0xffffffffu, !run || chok2);
       }
       // Every kAbortPairs pairs a screened neighbour checks the bound below.
       for (; t + 1 <= core_hi;) {
@@ -719,6 +726,12 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
       if (tr) {
         c_core1 = clock64();
         tr_noch = noch;
+      }
+    }
+    if (cool_noch) {
+      for (; t < T; ++t) {
+        if (t & 1) level(I1{}, PT{}, M2{}, t);
+        else level(I0{}, PT{}, M2{}, t);
       }
     }
     for (; t < T; ++t) pred_level(t);
@@ -784,23 +797,26 @@ __global__ void __launch_bounds__(256) k_eval(Bufs b, const Work* items, const i
 // evaluator class (the item's leaf selects the evaluator), so the long climbs
 // of one class overlap the bulk of the others instead of forming a serial
 // tail per class.
-// Two FIFO rings with ticket claims: level 0 (priority) receives the steps
-// of the critical leaves — the host's pick of the longest expected climbs
-// (P^2 M), as many as keep the ring within the resident warps, plus any leaf
-// whose climb so far is long (steps x levels per simulation >= hi_levels) —
-// level 1 everything else. The long climbs are the critical path: a step
-// waits for all of its items, so a climb behind a full ring advances one
-// ring's worth of items per step. Priority items run the lowest-latency
-// evaluator for their P (K = 4 up to P = 128: fewer stages per lane, a
-// shorter level) rather than the densest one. Each warp
-// holds at most one ticket per ring; it claims a priority ticket only when
-// the priority ring has unclaimed items, serves whichever of its tickets is
-// filled first, and keeps them across items (no CAS loops, no contention).
+// Three FIFO rings with ticket claims, in priority order: ring 0 receives
+// the steps of the critical leaves — the host's pick of the longest expected
+// climbs (P^2 M), as many as one warp per SM sub-partition can run — ring 1
+// those of any leaf whose climb so far is long (steps x levels per
+// simulation >= hi_levels), ring 2 everything else. The long climbs are the
+// critical path: a step waits for all of its items, so a climb queued behind
+// a full ring advances one ring's worth of items per step. Ring-0 items run
+// the lowest-latency evaluator for their P (K = 4 up to P = 128: fewer
+// stages per lane, a shorter level) and only warps 0-3 of each block serve
+// ring 0 (one per SM sub-partition). Each warp holds at most one ticket per
+// ring; it claims a ticket only when the ring has unclaimed items, serves
+// whichever of its tickets is filled first (never a lower ring while it
+// holds a higher one), and keeps them across items (no CAS loops).
+constexpr int kRings = 3;
+
 struct AsyncQ {
-  Work* slots[2];
-  unsigned long long* seq[2];   // slot k holds ticket t when seq[k] == t + 1
-  unsigned long long* head[2];  // next ticket to hand out
-  unsigned long long* tail[2];  // next ticket to produce
+  Work* slots[kRings];
+  unsigned long long* seq[kRings];   // slot k holds ticket t when seq[k] == t + 1
+  unsigned long long* head[kRings];  // next ticket to hand out
+  unsigned long long* tail[kRings];  // next ticket to produce
   int* pending;                 // per leaf: items of the current step not yet done
   int* active;                  // leaves still climbing
   int* abort;                   // watchdog flag
@@ -1384,8 +1400,8 @@ __device__ void advance_leaf(const Bufs& b, const AsyncQ& q, int li, int lane, b
     if (b.trace && b.trace_items && lane == 0) trace_event(b, 3, li, lf, n);
     if (n > 0) {
       const long long lv = (long long)__ldcg(&b.hs[li].steps) * (2 * (lf.M + lf.P - 1));
-      const bool hi = (q.crit && q.crit[li]) || lv >= q.hi_levels;
-      push_items(b, q, li, lf, hi ? 0 : 1, n, lane);
+      const int ring = (q.crit && q.crit[li]) ? 0 : (lv >= q.hi_levels ? 1 : 2);
+      push_items(b, q, li, lf, ring, n, lane);
       if (b.trace && b.trace_items && lane == 0) trace_event(b, 4, li, lf, 0);
       return;
     }
@@ -1421,17 +1437,25 @@ __device__ __forceinline__ bool try_slot(const AsyncQ& q, int lv, long long& tic
 // Lane 0: next item for this warp (see AsyncQ). Tickets are claimed only
 // when the ring shows unclaimed items, so an idle warp holds none.
 // Returns false when the warp should exit (no leaf climbing, or abort).
-__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[2], int lv0) {
+__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int lv0) {
   unsigned ns = 32;
   const long long t0 = clock64();
   for (;;) {
 #pragma unroll
-    for (int lv = 0; lv < 2; ++lv) {
+    bool held = false;
+    for (int lv = 0; lv < kRings; ++lv) {
       if (lv < lv0) continue;
+      // a claimed higher-priority ticket is being filled (the producer
+      // bumps the tail before it writes the slot): wait for it rather than
+      // start a long lower-priority item while holding it
+      if (held) break;
       if (tk[lv] < 0 &&
           *(volatile unsigned long long*)q.tail[lv] > *(volatile unsigned long long*)q.head[lv])
         tk[lv] = (long long)atomicAdd(q.head[lv], 1ULL);
       if (tk[lv] >= 0 && try_slot(q, lv, tk[lv], w)) return true;
+      // (a ticket past the tail — claimed in a race — waits for a future
+      // push and must not hold back the lower rings)
+      held = tk[lv] >= 0 && (unsigned long long)tk[lv] < *(volatile unsigned long long*)q.tail[lv];
     }
     const int act = *(volatile int*)q.active;
     if (act == 0 || *(volatile int*)q.abort) return false;
@@ -1440,7 +1464,7 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[2], int lv0) 
       atomicExch(q.abort, 1);
       return false;
     }
-    __nanosleep(ns);
+    __nanosleep(held ? 32 : ns);
     if (ns < 256) ns <<= 1;
   }
 }
@@ -1461,7 +1485,7 @@ __device__ __noinline__ void eval_item_call(const Bufs& b, const Work& w, int la
 
 __global__ void __launch_bounds__(256, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ q) {
   const int lane = threadIdx.x & 31;
-  long long tk[2] = {-1, -1};
+  long long tk[kRings] = {-1, -1, -1};
   for (;;) {
     int quit = 0, cls = 0;
     Work w{};
@@ -2238,7 +2262,12 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     if (leaves[k].mode != 0) continue;
     climb.push_back(k);
     int cls = hpk::eval_class(leaves[k].P, leaves[k].M, leaves[k].sched == 0);
-    int cpw = hpk::class_cpw(cls, leaves[k].P);
+    // a step's items at the denser of its two possible evaluators (priority
+    // items use lat_class): any ring holds at most one step per leaf, so this
+    // sum bounds every ring's fill and a ring can never wrap onto an
+    // unconsumed item
+    int cpw = std::min(hpk::class_cpw(cls, leaves[k].P),
+                       hpk::class_cpw(hpk::lat_class(leaves[k].P, cls), leaves[k].P));
     n_items += (2 * (leaves[k].P - 1) + cpw - 1) / cpw;
   }
   // Longest steps first: the seeding order is the initial queue order, so
@@ -2264,7 +2293,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     int* d_climb;
     if (!(s = upload(a, "climb_ids", climb, &d_climb)).ok()) return s;
     const size_t qcap = n_items + 1024;
-    for (int lv = 0; lv < 2; ++lv) {
+    for (int lv = 0; lv < hpk::kRings; ++lv) {
       std::string nm = "q_slots" + std::to_string(lv);
       if (!(s = scratch(a, nm.c_str(), qcap, &q.slots[lv])).ok()) return s;
       nm = "q_seq" + std::to_string(lv);
@@ -2276,11 +2305,13 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     CK(cudaMemsetAsync(d_q, 0, 8 * sizeof(unsigned long long), st));
     q.head[0] = d_q;
     q.head[1] = d_q + 1;
-    q.tail[0] = d_q + 2;
-    q.tail[1] = d_q + 3;
-    q.active = reinterpret_cast<int*>(d_q + 4);
+    q.head[2] = d_q + 2;
+    q.tail[0] = d_q + 3;
+    q.tail[1] = d_q + 4;
+    q.tail[2] = d_q + 5;
+    q.active = reinterpret_cast<int*>(d_q + 6);
     q.cap = qcap;
-    q.hi_levels = 1LL << 20;
+    q.hi_levels = 1LL << 17;
     if (const char* e = std::getenv("HP_HI_LEVELS")) q.hi_levels = std::atoll(e);  // tuning
     int threads = 256;
     if (const char* e = std::getenv("HP_ASYNC_THREADS")) threads = std::atoi(e);  // tuning
@@ -2339,7 +2370,16 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     int abort_flag = 0;
     CK(cudaMemcpyAsync(&abort_flag, q.abort, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (abort_flag) return hph::Status{HP_INTERNAL, "watchdog: hill-climb work queue stalled"};
+    if (abort_flag) {
+      // ring counters for the report: head/tail per ring, leaves climbing
+      unsigned long long ctr[7] = {0, 0, 0, 0, 0, 0, 0};
+      cudaMemcpy(ctr, q.head[0], sizeof ctr, cudaMemcpyDeviceToHost);
+      char msg[256];
+      std::snprintf(msg, sizeof msg,
+                    "watchdog: hill-climb work queue stalled (head %llu/%llu/%llu tail %llu/%llu/%llu active %d)",
+                    ctr[0], ctr[1], ctr[2], ctr[3], ctr[4], ctr[5], (int)(ctr[6] & 0xffffffffu));
+      return hph::Status{HP_INTERNAL, msg};
+    }
   }
 
   // ---- exhaustive leaves: bounded compositions only (memory gate solved

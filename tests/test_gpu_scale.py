@@ -64,3 +64,40 @@ def test_shard_reduction_invariance(engine, count):
         assert (red.candidates_simulated, red.candidates_pruned) == (whole.candidates_simulated,
                                                                      whole.candidates_pruned)
         assert abi.encode_plan(p.group_names, red.best_plan) == abi.encode_plan(p.group_names, whole.best_plan)
+
+
+SCHED_KNOBS = [
+    {},
+    {"HP_CRIT_WARPS": "0"},                      # no critical leaves: rings 1/2 only
+    {"HP_HI_LEVELS": "1000000000000"},           # no long-climber ring
+    {"HP_NO_LEAD": "1", "HP_NO_LAT": "1"},       # priority ring served by every warp, dense evaluator
+    {"HP_CRIT_WARPS": "100000", "HP_HI_LEVELS": "1"},  # (almost) everything prioritised
+    {"HP_ASYNC_THREADS": "128"},                 # 4 warps per block
+]
+
+
+@pytest.mark.parametrize("knobs", SCHED_KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "default")
+def test_climb_scheduling_does_not_change_results(engine, knobs):
+    """The climb kernel's scheduling (critical leaves, priority rings, lead
+    warps, latency evaluator, block size; read per search from the
+    environment) may only change the order in which items run: counts, time
+    and plan must be identical, with and without the search log, on C3
+    subsets with long climbs (pp 12 and 88-96)."""
+    cfg = configs.with_pp(configs.config("C3", full=True), [12, 88, 92, 96])
+    p = abi.Problem(cfg)
+    old = {k: os.environ.get(k) for k in knobs}
+    os.environ.update(knobs)
+    try:
+        r = engine.search_shard(p)
+        rl = engine.search_shard(p, flags=abi.HP_FLAG_LOG)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    ref = engine.search_shard(p)
+    for x in (r, rl):
+        assert (x.candidates_simulated, x.candidates_pruned) == (ref.candidates_simulated, ref.candidates_pruned)
+        assert x.best_time_s == ref.best_time_s
+        assert abi.encode_plan(p.group_names, x.best_plan) == abi.encode_plan(p.group_names, ref.best_plan)
