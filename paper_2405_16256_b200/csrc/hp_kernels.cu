@@ -675,9 +675,20 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
       for (; t + 1 <= core_hi;) {
         const int stop = min(core_hi - 1, t + 2 * kAbortPairs - 2);
         if (noch) {
-          for (; t <= stop; t += 2) {
-            level(I0{}, PF{}, M2{}, t);
-            level(I1{}, PF{}, M2{}, t + 1);
+          // unrolled so the scheduler can overlap the tail of one level pair
+          // with the next (deeper for K = 4, the latency evaluator)
+          if constexpr (K == 4) {
+#pragma unroll 4
+            for (; t <= stop; t += 2) {
+              level(I0{}, PF{}, M2{}, t);
+              level(I1{}, PF{}, M2{}, t + 1);
+            }
+          } else {
+#pragma unroll 2
+            for (; t <= stop; t += 2) {
+              level(I0{}, PF{}, M2{}, t);
+              level(I1{}, PF{}, M2{}, t + 1);
+            }
           }
         } else {
           for (; t <= stop; t += 2) {
