@@ -611,12 +611,19 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
     using M0 = std::integral_constant<int, 0>;
     using M1 = std::integral_constant<int, 1>;
     using M2 = std::integral_constant<int, 2>;
-    auto pred_level = [&](int t) {
-      if (t & 1) level(I1{}, PT{}, M0{}, t);
-      else level(I0{}, PT{}, M0{}, t);
-    };
     int t = P;
-    for (; t < T && t < core_lo; ++t) pred_level(t);
+    // predicated levels [t, t1) in (even, odd) pairs, so the two parities
+    // are compile-time and the scheduler sees two levels at a time
+    auto pred_range = [&](auto mode_tag, int t1) {
+      if (t < t1 && (t & 1)) level(I1{}, PT{}, mode_tag, t++);
+#pragma unroll 1
+      for (; t + 1 < t1; t += 2) {
+        level(I0{}, PT{}, mode_tag, t);
+        level(I1{}, PT{}, mode_tag, t + 1);
+      }
+      if (t < t1) level(I0{}, PT{}, mode_tag, t++);
+    };
+    pred_range(M0{}, min(T, core_lo));
     bool cool_noch = false;  // cool-down without channel maxima (below)
     if (core_lo <= core_hi) {
       // core_lo is even: pairs (even, odd), then the final even level.
@@ -739,13 +746,8 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
         tr_noch = noch;
       }
     }
-    if (cool_noch) {
-      for (; t < T; ++t) {
-        if (t & 1) level(I1{}, PT{}, M2{}, t);
-        else level(I0{}, PT{}, M2{}, t);
-      }
-    }
-    for (; t < T; ++t) pred_level(t);
+    if (cool_noch) pred_range(M2{}, T);
+    else pred_range(M0{}, T);
   }
   if (tr) {
     trace_cycles(b, 5, w.leaf, P, M, tr_noch ? 1 : 0, c_core1 - c_core0);
