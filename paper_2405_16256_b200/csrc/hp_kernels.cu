@@ -713,13 +713,35 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
           // iteration time (evaluate.cpp:90-97). A neighbour above the
           // current point's time can neither be the move nor tie the leaf
           // best (nb_screen), so it stops here as T_SKIP.
+          // Drain: stage i's last op is B(i, M-1), whose gradient still
+          // travels down to stage 0 (send j -> j-1, then B(j-1, M-1)), so
+          // compute_end_0 >= compute_end_i + sum_{k<i} (sf_k + b_k) and the
+          // iteration is >= that + dps_0 (sim.cpp:127-141, evaluate.cpp:90-97).
+          // Summed in another order than the simulation; the margin absorbs it.
+          double dr[K];
+          double acc = 0.0;
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const int i = sl * K + r;
+            dr[r] = acc;
+            if (run && i < P - 1) acc = acc + (sf[r] + bw[r]);
+          }
+          double ex = acc;
+          for (int off = 1; off < W; off <<= 1) {
+            const double o = __shfl_up_sync(0xffffffffu, ex, off);
+            if (sl >= off) ex = ex + o;
+          }
+          ex = __shfl_up_sync(0xffffffffu, ex, 1);
+          if (sl == 0) ex = 0.0;
+          const double dps0 = dmax(__shfl_sync(0xffffffffu, dps[0], min(31, seg * W)), 0.0);
           double lb = NEG;
 #pragma unroll
           for (int r = 0; r < K; ++r) {
             const int i = sl * K + r;
             if (run && i < P) {
               const int nf = min(M, (t - 1 - i) / 2 + 1), nbk = min(M, (t - 2 * P + i) / 2 + 1);
-              lb = dmax(lb, fr[r] + ((double)(M - nf) * f[r] + (double)(M - nbk) * bw[r]) + dps[r]);
+              const double tail = dmax(dps[r], (ex + dr[r]) + dps0);
+              lb = dmax(lb, fr[r] + ((double)(M - nf) * f[r] + (double)(M - nbk) * bw[r]) + tail);
             }
           }
           for (int off = 1; off < W; off <<= 1) {
