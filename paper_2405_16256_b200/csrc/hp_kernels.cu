@@ -1512,13 +1512,18 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int 
 #ifndef HP_ALL_MINB
 #define HP_ALL_MINB 1
 #endif
+// threads per block of the climb kernel (tuning: 384 = 12 warps per SM at
+// <= 168 registers)
+#ifndef HP_ASYNC_MAXT
+#define HP_ASYNC_MAXT 256
+#endif
 
 template <int K, bool FAST>
 __device__ __noinline__ void eval_item_call(const Bufs& b, const Work& w, int lane) {
   eval_item<K, FAST>(b, w, lane);
 }
 
-__global__ void __launch_bounds__(256, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ q) {
+__global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ q) {
   const int lane = threadIdx.x & 31;
   long long tk[kRings] = {-1, -1, -1};
   for (;;) {
@@ -2348,7 +2353,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     q.cap = qcap;
     q.hi_levels = 1LL << 17;
     if (const char* e = std::getenv("HP_HI_LEVELS")) q.hi_levels = std::atoll(e);  // tuning
-    int threads = 256;
+    int threads = HP_ASYNC_MAXT;
     if (const char* e = std::getenv("HP_ASYNC_THREADS")) threads = std::atoi(e);  // tuning
     const int grid = async_grid(a.sm_count, threads);
     q.lat = std::getenv("HP_NO_LAT") ? 0 : 1;  // tuning
