@@ -198,6 +198,8 @@ def main_ours(args):
             raise SystemExit("--gpus N > 1 must be launched with torchrun (one rank per GPU)")
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's banner / debug log goes to stderr: stdout carries only the JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     docs = configs.config(args.config, full=True)
     eng = planner.engine(local)
