@@ -177,7 +177,7 @@ def main_reference(args):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": jobs if kind == "reference" else 1,
                              "kind": kind, "sample": f"C3 full sweep, pipeline degrees {CPU_SAMPLE_PP}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -198,8 +198,6 @@ def main_ours(args):
             raise SystemExit("--gpus N > 1 must be launched with torchrun (one rank per GPU)")
     torch.cuda.set_device(local)
     if world > 1:
-        # NCCL's banner / debug log goes to stderr: stdout carries only the JSON line
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     docs = configs.config(args.config, full=True)
     eng = planner.engine(local)
@@ -328,13 +326,29 @@ def main_ours(args):
             line["cpu_baseline"] = cb
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "error": str(e)}
-    print(json.dumps(line), flush=True)
+    emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # Libraries (NCCL's version banner, CUDA, the engine) may write to fd 1;
+    # send all of that to stderr so stdout carries only the JSON line.
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         return main_reference(args)

@@ -141,6 +141,7 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   else mine = hph::shard_leaves(p, shard, nshard);
   result->host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
   ctx->arena.time_evals = opts && (opts->flags & HP_FLAG_TIME_KERNELS);
+  ctx->arena.shard_count = nshard;
   const bool want_log = opts && (opts->flags & HP_FLAG_LOG);
   ctx->log.clear();
   ctx->arena.log.reset();

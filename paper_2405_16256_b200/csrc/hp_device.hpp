@@ -68,6 +68,7 @@ struct Arena {
 
   // optional per-launch timing of the evaluator kernels (bench roofline)
   bool time_evals = false;
+  int shard_count = 1;  // shards of the whole search (climb scheduling policy only)
   double h2d_bytes = 0.0, d2h_bytes = 0.0;  // per search
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;

@@ -860,6 +860,10 @@ struct AsyncQ {
   const unsigned char* crit;    // per leaf: critical (level 0 from the first step)
   int lat;                      // level-0 items use lat_class
   int lead;                     // level 0 is served by warps 0-3 of each block only
+  int crit_sms;                 // > 0: level 0 only on the first crit_sms blocks (one per SM),
+                                // whose warps 4-7 exit: critical items run alone on their
+                                // sub-partitions (see k_hill_async)
+  int r1_thr;                   // see pop_item (0: every warp serves ring 1)
 };
 
 __device__ __forceinline__ int leaf_class(const Leaf& lf) { return eval_class(lf.P, lf.M, lf.sched == 0); }
@@ -1472,7 +1476,7 @@ __device__ __forceinline__ bool try_slot(const AsyncQ& q, int lv, long long& tic
 // Lane 0: next item for this warp (see AsyncQ). Tickets are claimed only
 // when the ring shows unclaimed items, so an idle warp holds none.
 // Returns false when the warp should exit (no leaf climbing, or abort).
-__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int lv0) {
+__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int lv0, bool lead) {
   unsigned ns = 32;
   const long long t0 = clock64();
   for (;;) {
@@ -1484,8 +1488,11 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int 
       // bumps the tail before it writes the slot): wait for it rather than
       // start a long lower-priority item while holding it
       if (held) break;
-      if (tk[lv] < 0 &&
-          *(volatile unsigned long long*)q.tail[lv] > *(volatile unsigned long long*)q.head[lv])
+      // (r1_thr > 0: a non-lead warp takes a long-climber item only from a
+      // backlog above r1_thr, so a thin ring 1 runs one item per sub-partition)
+      const unsigned long long tl = *(volatile unsigned long long*)q.tail[lv];
+      const unsigned long long hd = *(volatile unsigned long long*)q.head[lv];
+      if (tk[lv] < 0 && tl > hd && (lv != 1 || lead || tl - hd > (unsigned long long)q.r1_thr))
         tk[lv] = (long long)atomicAdd(q.head[lv], 1ULL);
       if (tk[lv] >= 0 && try_slot(q, lv, tk[lv], w)) return true;
       // (a ticket past the tail — claimed in a race — waits for a future
@@ -1526,6 +1533,7 @@ __device__ __noinline__ void eval_item_call(const Bufs& b, const Work& w, int la
 __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ q) {
   const int lane = threadIdx.x & 31;
   long long tk[kRings] = {-1, -1, -1};
+  if (q.crit_sms > 0 && (int)blockIdx.x < q.crit_sms && (threadIdx.x >> 5) >= 4) return;
   for (;;) {
     int quit = 0, cls = 0;
     Work w{};
@@ -1533,7 +1541,10 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
       // priority items go to one warp per SM sub-partition (warps 0-3 of
       // the SM's one block), so two of them never share one: a climb step
       // waits for its slowest item
-      quit = pop_item(q, w, tk, (threadIdx.x >> 5) < 4 || !q.lead ? 0 : 1) ? 0 : 1;
+      const int wib = threadIdx.x >> 5;
+      int lv0 = wib < 4 || !q.lead ? 0 : 1;
+      if (q.crit_sms > 0) lv0 = (int)blockIdx.x < q.crit_sms ? 0 : 1;
+      quit = pop_item(q, w, tk, lv0, wib < 4) ? 0 : 1;
       if (!quit) cls = w.out > 0 ? w.out - 1 : leaf_class(b.leaves[w.leaf]);
     }
     quit = __shfl_sync(0xffffffffu, quit, 0);
@@ -2352,6 +2363,8 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     q.active = reinterpret_cast<int*>(d_q + 6);
     q.cap = qcap;
     q.hi_levels = 1LL << 17;
+    q.r1_thr = 0;
+    if (const char* e = std::getenv("HP_R1_THR")) q.r1_thr = std::max(0, std::atoi(e));  // tuning
     if (const char* e = std::getenv("HP_HI_LEVELS")) q.hi_levels = std::atoll(e);  // tuning
     int threads = HP_ASYNC_MAXT;
     if (const char* e = std::getenv("HP_ASYNC_THREADS")) threads = std::atoi(e);  // tuning
@@ -2362,7 +2375,13 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     // resident warps
     {
       q.lead = (threads >= 128 && !std::getenv("HP_NO_LEAD")) ? 1 : 0;  // tuning
-      long long budget = (long long)grid * (q.lead ? 4 : threads / 32);
+      // A shard of a 4+-GPU sweep ends on its critical climbs, not its bulk:
+      // give them half of the SMs alone (C3 on 4 GPUs 128 -> 123 ms; on one
+      // GPU the bulk dominates and the reservation costs 242 -> 275 ms).
+      q.crit_sms = a.shard_count >= 4 ? grid / 2 : 0;
+      if (const char* e = std::getenv("HP_CRIT_SMS")) q.crit_sms = std::min(grid, std::max(0, std::atoi(e)));  // tuning
+      if (q.crit_sms > 0) q.lead = 1;
+      long long budget = (long long)(q.crit_sms > 0 ? q.crit_sms : grid) * (q.lead ? 4 : threads / 32);
       if (const char* e = std::getenv("HP_CRIT_WARPS")) budget = std::atoll(e);  // tuning
       std::vector<int> byest(climb);
       std::stable_sort(byest.begin(), byest.end(), [&](int x, int y) {
