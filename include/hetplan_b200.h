@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define HP_ABI_VERSION 1
+#define HP_ABI_VERSION 2
 #define HP_MAX_GROUPS 8      /* device groups (accelerator types) per cluster */
 #define HP_MAX_STAGES 256    /* pipeline stages per plan */
 #define HP_NAME_LEN 32
@@ -196,6 +196,16 @@ typedef struct hp_result {
   double host_ms;          /* host enumeration + table build time */
   int32_t hill_iterations; /* steepest-descent rounds */
   int32_t _pad1;
+  /* Device work behind candidates_simulated (which counts like the
+   * reference): candidates simulated to the end on the GPU, simulations
+   * stopped early by the admissible lower bound, and candidates that bound
+   * excluded before any simulation. The bound only removes candidates whose
+   * time can neither be the hill-climb move nor tie the leaf best, so
+   * decisions, counts and the winner are the reference's. Memo hits the GPU
+   * re-evaluates are included here but not in candidates_simulated. */
+  int64_t device_simulated;
+  int64_t device_aborted;
+  int64_t device_screened;
   hp_plan best_plan;
 } hp_result;
 

@@ -57,7 +57,7 @@ def lib():
 
 
 def abi_version() -> int:
-    return 1
+    return 2
 
 
 EXPORTED = ["hp_abi_version", "hp_create", "hp_destroy", "hp_last_error", "hp_validate", "hp_probe",

@@ -91,7 +91,8 @@ class hp_result(C.Structure):
                 ("global_bound", C.c_double), ("device_ms", C.c_double), ("gpu_launches", C.c_int64),
                 ("eval_launches", C.c_int64), ("eval_ms", C.c_double), ("eval_fp64_ops", C.c_double),
                 ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double), ("host_ms", C.c_double),
-                ("hill_iterations", C.c_int32), ("_pad1", C.c_int32), ("best_plan", hp_plan)]
+                ("hill_iterations", C.c_int32), ("_pad1", C.c_int32), ("device_simulated", C.c_int64),
+                ("device_aborted", C.c_int64), ("device_screened", C.c_int64), ("best_plan", hp_plan)]
 
 
 class hp_log_entry(C.Structure):

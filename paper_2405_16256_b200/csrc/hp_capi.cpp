@@ -43,6 +43,38 @@ hp_status prepare(hp_ctx* ctx, const hp_problem* problem, hph::Problem& p) {
   return HP_OK;
 }
 
+// The plans hp_evaluate_plans / hp_evaluate_plan_full accept: the shapes
+// evaluate_plan_unchecked (evaluate.cpp:23-107) gives a meaning, checked so
+// the device's stage-index edge test (hp_core.cuh stage_compute) is the
+// reference's layer_range test (begin == 0 / end == num_layers): stages
+// cover [0, num_layers) contiguously, each non-empty (an empty or inverted
+// range is what makes simulate reject negative stage times, sim.cpp:66-73).
+hph::Status check_plan_shape(const hph::Problem& p, const hp_plan& pl) {
+  auto bad = [](const std::string& m) { return hph::Status{HP_BAD_CONFIG, m}; };
+  if (pl.n_stages < 1 || pl.n_stages > HP_MAX_STAGES) return bad("plan: bad stage count");
+  if (pl.schedule != HP_GPIPE && pl.schedule != HP_1F1B) return bad("plan: unknown schedule");
+  if (pl.micro_batches_per_dp_replica < 1) return bad("simulate: micro_batches must be >= 1");
+  if (pl.micro_batches_per_dp_replica > 5000000) return bad("simulate: micro_batches too large");
+  int next = 0;
+  for (int i = 0; i < pl.n_stages; ++i) {
+    const hp_stage& st = pl.stages[i];
+    if (st.layer_begin != next || st.layer_end <= st.layer_begin)
+      return bad("plan: stage " + std::to_string(i) + " layer range [" + std::to_string(st.layer_begin) + ", " +
+                 std::to_string(st.layer_end) + ") does not continue the previous stage");
+    next = st.layer_end;
+    if (st.group < 0 || st.group >= static_cast<int>(p.groups.size())) return bad("plan: unknown device group");
+    if (st.tp_degree < 1) return bad("compute_time: tp_degree must be >= 1");
+    if (st.dp_degree < 1) return bad("plan: dp_degree must be >= 1");
+    if (i + 1 < pl.n_stages && st.group != pl.stages[i + 1].group &&
+        p.pair[st.group][pl.stages[i + 1].group] < 0)
+      return bad("no link between stages " + std::to_string(i) + " and " + std::to_string(i + 1));
+  }
+  if (next != p.model.num_layers)
+    return bad("plan: stages cover " + std::to_string(next) + " of " + std::to_string(p.model.num_layers) +
+               " layers");
+  return hph::Status{};
+}
+
 }  // namespace
 
 extern "C" {
@@ -183,6 +215,9 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   result->h2d_bytes = out.h2d_bytes;
   result->d2h_bytes = out.d2h_bytes + sizeof(hp_result);
   result->hill_iterations = out.hill_iterations;
+  result->device_simulated = out.dev_simulated;
+  result->device_aborted = out.dev_aborted;
+  result->device_screened = out.dev_screened;
   result->global_bound = p.pruning ? out.global_bound : std::numeric_limits<double>::infinity();
   if (p.pruning) {
     long long nl = 0;
@@ -248,19 +283,8 @@ hp_status hp_evaluate_plans(hp_ctx* ctx, const hp_problem* problem, const hp_pla
   if (!s.ok()) return fail(ctx, s);
   if (n < 0 || (n > 0 && (!plans || !iteration_time_s))) return fail(ctx, HP_BAD_CONFIG, "bad plan array");
   for (int k = 0; k < n; ++k) {
-    const hp_plan& pl = plans[k];
-    if (pl.n_stages < 1 || pl.n_stages > HP_MAX_STAGES) return fail(ctx, HP_BAD_CONFIG, "plan: bad stage count");
-    if (pl.micro_batches_per_dp_replica < 1) return fail(ctx, HP_BAD_CONFIG, "simulate: micro_batches must be >= 1");
-    if (pl.micro_batches_per_dp_replica > 5000000) return fail(ctx, HP_BAD_CONFIG, "simulate: micro_batches too large");
-    for (int i = 0; i < pl.n_stages; ++i) {
-      const hp_stage& st = pl.stages[i];
-      if (st.group < 0 || st.group >= static_cast<int>(p.groups.size()))
-        return fail(ctx, HP_BAD_CONFIG, "plan: unknown device group");
-      if (st.tp_degree < 1) return fail(ctx, HP_BAD_CONFIG, "compute_time: tp_degree must be >= 1");
-      if (i + 1 < pl.n_stages && st.group != pl.stages[i + 1].group &&
-          p.pair[st.group][pl.stages[i + 1].group] < 0)
-        return fail(ctx, HP_BAD_CONFIG, "no link between stages " + std::to_string(i) + " and " + std::to_string(i + 1));
-    }
+    hph::Status c = check_plan_shape(p, plans[k]);
+    if (!c.ok()) return fail(ctx, c);
   }
   s = hpd::evaluate_plans(ctx->arena, p, plans, n, iteration_time_s);
   return s.ok() ? HP_OK : fail(ctx, s);

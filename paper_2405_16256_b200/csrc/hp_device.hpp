@@ -138,6 +138,11 @@ struct SearchOut {
   long long eval_launches = 0;
   double eval_ms = 0.0;        // summed evaluator kernel time (when timed)
   double eval_fp64_ops = 0.0;  // algorithmic FP64 add/max ops simulated
+  // device work behind the counts: candidates simulated to the end, stopped
+  // early by the admissible bound, and excluded by it before simulation
+  // (the latter two are counted as simulated, like the reference, which
+  // simulates them; their times cannot win or tie)
+  long long dev_simulated = 0, dev_aborted = 0, dev_screened = 0;
   double h2d_bytes = 0.0, d2h_bytes = 0.0;
 };
 

@@ -356,7 +356,10 @@ __device__ __forceinline__ void eval_item_generic(const Bufs& b, const Work& w, 
       if (w.kind == 0) b.tseed[2 * w.leaf + (int)cand_id(w, seg)] = t;
       else if (w.kind == 1) b.nb[b.nb_off[w.leaf] + (int)cand_id(w, seg)] = t;
       else b.xbuf[w.out + seg] = t;
-      if (run && b.ops) atomicAdd(b.ops, (unsigned long long)(8LL * P * M - 4LL * M));
+      if (run && b.ops) {
+        atomicAdd(b.ops, (unsigned long long)(8LL * P * M - 4LL * M));
+        atomicAdd(b.ops + 1, 1ULL);
+      }
     }
   }
 }
@@ -797,7 +800,10 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
     else b.xbuf[w.out + seg] = tt;
     // algorithmic ops of the levels this candidate needed
     const long long full = 8LL * P * M - 4LL * M;
-    if (run && b.ops) atomicAdd(b.ops, (unsigned long long)(dead ? full * dead_t / (2LL * (M + P - 1)) : full));
+    if (run && b.ops) {
+      atomicAdd(b.ops, (unsigned long long)(dead ? full * dead_t / (2LL * (M + P - 1)) : full));
+      atomicAdd(b.ops + (dead ? 2 : 1), 1ULL);
+    }
   }
 }
 
@@ -841,10 +847,14 @@ __global__ void __launch_bounds__(256) k_eval(Bufs b, const Work* items, const i
 // a full ring advances one ring's worth of items per step. Ring-0 items run
 // the lowest-latency evaluator for their P (K = 4 up to P = 128: fewer
 // stages per lane, a shorter level) and only warps 0-3 of each block serve
-// ring 0 (one per SM sub-partition). Each warp holds at most one ticket per
-// ring; it claims a ticket only when the ring has unclaimed items, serves
-// whichever of its tickets is filled first (never a lower ring while it
-// holds a higher one), and keeps them across items (no CAS loops).
+// ring 0 (one per SM sub-partition). A warp claims a ticket only below the
+// ring's tail (CAS on head), so every claimed ticket has been pushed and its
+// slot is read right after the producer's write lands: no warp holds a
+// ticket across items. The slots a ring can have unread are then its
+// unclaimed items plus one per resident warp, both bounded by the ring
+// capacity (one step per climbing leaf, plus the resident warps), so the
+// producer never laps an unread slot; a consumer that finds its slot's
+// sequence number past its ticket reports the overwrite instead of hanging.
 constexpr int kRings = 3;
 
 struct AsyncQ {
@@ -854,7 +864,8 @@ struct AsyncQ {
   unsigned long long* tail[kRings];  // next ticket to produce
   int* pending;                 // per leaf: items of the current step not yet done
   int* active;                  // leaves still climbing
-  int* abort;                   // watchdog flag
+  int* abort;                   // 1: watchdog (no global progress), 2: ring overwrite
+  unsigned long long* progress; // items completed (global progress for the watchdog)
   unsigned long long cap;
   long long hi_levels;          // priority threshold (see above)
   const unsigned char* crit;    // per leaf: critical (level 0 from the first step)
@@ -1077,6 +1088,7 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
   // then the survivor list in slot order
   constexpr int NQ = (2 * HP_MAX_STAGES + 31) / 32;
   unsigned sv = 0;
+  int nskip = 0;
 #pragma unroll
   for (int j = 0; j < NQ; ++j) {
     const int qq = 32 * j + lane;
@@ -1084,8 +1096,11 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
       const double scr = screen ? nb_screen_pre(lf, sl, sn, qq, cur_t) : 0.0;
       if (scr == 0.0) sv |= 1u << j;
       else nbt[qq] = scr;
+      nskip += scr == T_SKIP ? 1 : 0;
     }
   }
+  nskip = __reduce_add_sync(0xffffffffu, (unsigned)nskip);
+  if (lane == 0 && nskip && b.ops) atomicAdd(b.ops + 3, (unsigned long long)nskip);
   int n = 0;
   for (int j = 0; 32 * j < nslots; ++j) {
     const bool surv = (sv >> j) & 1u;
@@ -1458,10 +1473,18 @@ __global__ void k_async_seed(Bufs b, AsyncQ q, const int* ids, int n) {
   advance_leaf(b, q, li, lane, false);
 }
 
-__device__ __forceinline__ bool try_slot(const AsyncQ& q, int lv, long long& ticket, Work& w) {
-  const unsigned long long h = (unsigned long long)ticket;
+// Reads the item of a claimed ticket (below the tail: the producer has
+// bumped the tail and is writing or has written the slot). Returns false
+// when the slot was lapped (its sequence number is past the ticket), which
+// the ring sizing rules out; the caller aborts the search loudly.
+__device__ __forceinline__ bool read_slot(const AsyncQ& q, int lv, unsigned long long h, Work& w) {
   const unsigned long long k = h % q.cap;
-  if (*(volatile unsigned long long*)(q.seq[lv] + k) != h + 1) return false;
+  for (;;) {
+    const unsigned long long s = *(volatile unsigned long long*)(q.seq[lv] + k);
+    if (s == h + 1) break;
+    if (s > h + 1) return false;
+    __nanosleep(20);
+  }
   __threadfence();
   const Work* sl = q.slots[lv] + k;
   w.leaf = __ldcg(&sl->leaf);
@@ -1469,44 +1492,55 @@ __device__ __forceinline__ bool try_slot(const AsyncQ& q, int lv, long long& tic
   w.first = __ldcg(&sl->first);
   w.n = __ldcg(&sl->n);
   w.out = __ldcg(&sl->out);
-  ticket = -1;
   return true;
 }
 
-// Lane 0: next item for this warp (see AsyncQ). Tickets are claimed only
-// when the ring shows unclaimed items, so an idle warp holds none.
-// Returns false when the warp should exit (no leaf climbing, or abort).
-__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int lv0, bool lead) {
-  unsigned ns = 32;
-  const long long t0 = clock64();
+// Claims the next ticket of ring lv if one is below the tail.
+__device__ __forceinline__ bool claim(const AsyncQ& q, int lv, bool lead, unsigned long long& ticket) {
+  unsigned long long hd = *(volatile unsigned long long*)q.head[lv];
   for (;;) {
-#pragma unroll
-    bool held = false;
-    for (int lv = 0; lv < kRings; ++lv) {
-      if (lv < lv0) continue;
-      // a claimed higher-priority ticket is being filled (the producer
-      // bumps the tail before it writes the slot): wait for it rather than
-      // start a long lower-priority item while holding it
-      if (held) break;
-      // (r1_thr > 0: a non-lead warp takes a long-climber item only from a
-      // backlog above r1_thr, so a thin ring 1 runs one item per sub-partition)
-      const unsigned long long tl = *(volatile unsigned long long*)q.tail[lv];
-      const unsigned long long hd = *(volatile unsigned long long*)q.head[lv];
-      if (tk[lv] < 0 && tl > hd && (lv != 1 || lead || tl - hd > (unsigned long long)q.r1_thr))
-        tk[lv] = (long long)atomicAdd(q.head[lv], 1ULL);
-      if (tk[lv] >= 0 && try_slot(q, lv, tk[lv], w)) return true;
-      // (a ticket past the tail — claimed in a race — waits for a future
-      // push and must not hold back the lower rings)
-      held = tk[lv] >= 0 && (unsigned long long)tk[lv] < *(volatile unsigned long long*)q.tail[lv];
+    const unsigned long long tl = *(volatile unsigned long long*)q.tail[lv];
+    // (r1_thr > 0: a non-lead warp takes a long-climber item only from a
+    // backlog above r1_thr, so a thin ring 1 runs one item per sub-partition)
+    if (!(tl > hd && (lv != 1 || lead || tl - hd > (unsigned long long)q.r1_thr))) return false;
+    const unsigned long long old = atomicCAS(q.head[lv], hd, hd + 1);
+    if (old == hd) {
+      ticket = hd;
+      return true;
+    }
+    hd = old;
+  }
+}
+
+// Lane 0: next item for this warp (see AsyncQ), highest-priority ring first.
+// Returns false when the warp should exit (no leaf climbing, or abort).
+__device__ bool pop_item(const AsyncQ& q, Work& w, int lv0, bool lead) {
+  unsigned ns = 32;
+  long long t0 = clock64();
+  unsigned long long seen = *(volatile unsigned long long*)q.progress;
+  for (;;) {
+    for (int lv = lv0; lv < kRings; ++lv) {
+      unsigned long long tk;
+      if (claim(q, lv, lead, tk)) {
+        if (read_slot(q, lv, tk, w)) return true;
+        atomicExch(q.abort, 2);
+        return false;
+      }
     }
     const int act = *(volatile int*)q.active;
     if (act == 0 || *(volatile int*)q.abort) return false;
-    // watchdog: ~30 s without work while leaves are active means a bug
-    if (clock64() - t0 > (1LL << 36)) {
+    // watchdog: no item completed anywhere for ~35 s while leaves are
+    // active means a lost item (a single item takes at most ~1e9 cycles:
+    // 2(M+P-1) levels with M <= 5e6)
+    const unsigned long long pg = *(volatile unsigned long long*)q.progress;
+    if (pg != seen) {
+      seen = pg;
+      t0 = clock64();
+    } else if (clock64() - t0 > (1LL << 36)) {
       atomicExch(q.abort, 1);
       return false;
     }
-    __nanosleep(held ? 32 : ns);
+    __nanosleep(ns);
     if (ns < 256) ns <<= 1;
   }
 }
@@ -1532,7 +1566,6 @@ __device__ __noinline__ void eval_item_call(const Bufs& b, const Work& w, int la
 
 __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ q) {
   const int lane = threadIdx.x & 31;
-  long long tk[kRings] = {-1, -1, -1};
   if (q.crit_sms > 0 && (int)blockIdx.x < q.crit_sms && (threadIdx.x >> 5) >= 4) return;
   for (;;) {
     int quit = 0, cls = 0;
@@ -1544,7 +1577,7 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
       const int wib = threadIdx.x >> 5;
       int lv0 = wib < 4 || !q.lead ? 0 : 1;
       if (q.crit_sms > 0) lv0 = (int)blockIdx.x < q.crit_sms ? 0 : 1;
-      quit = pop_item(q, w, tk, lv0, wib < 4) ? 0 : 1;
+      quit = pop_item(q, w, lv0, wib < 4) ? 0 : 1;
       if (!quit) cls = w.out > 0 ? w.out - 1 : leaf_class(b.leaves[w.leaf]);
     }
     quit = __shfl_sync(0xffffffffu, quit, 0);
@@ -1576,6 +1609,7 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
       __threadfence();
       last = atomicSub(q.pending + w.leaf, 1) == 1;
       if (last) __threadfence();
+      atomicAdd(q.progress, 1ULL);
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) advance_leaf(b, q, w.leaf, lane, true);
@@ -1900,7 +1934,11 @@ __global__ void __launch_bounds__(128) k_exh_thread(Bufs b, const ExhItem* items
   }
   if (lane == 0) {
     recs[it] = ExhRec{bt, brank, sim, w.leaf, brank >= 0 ? 1 : 0};
-    if (b.ops) atomicAdd(b.ops, (unsigned long long)ran * (unsigned long long)(8LL * P * lf.M - 4LL * lf.M));
+    if (b.ops) {
+      atomicAdd(b.ops, (unsigned long long)ran * (unsigned long long)(8LL * P * lf.M - 4LL * lf.M));
+      atomicAdd(b.ops + 1, (unsigned long long)ran);
+      atomicAdd(b.ops + 3, (unsigned long long)(sim - ran));
+    }
   }
 }
 
@@ -2240,8 +2278,8 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   int* d_ctr;
   if (!(s = scratch(a, "ctr", 32, &d_ctr)).ok()) return s;
   unsigned long long* d_ops;
-  if (!(s = scratch(a, "ops", 1, &d_ops)).ok()) return s;
-  CK(cudaMemsetAsync(d_ops, 0, sizeof(unsigned long long), st));
+  if (!(s = scratch(a, "ops", 4, &d_ops)).ok()) return s;
+  CK(cudaMemsetAsync(d_ops, 0, 4 * sizeof(unsigned long long), st));
   b.ops = d_ops;
   const int grid = a.sm_count * 8;
   const int T = 128;
@@ -2343,7 +2381,9 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     if (!(s = scratch(a, "q_pending", nL, &q.pending)).ok()) return s;
     int* d_climb;
     if (!(s = upload(a, "climb_ids", climb, &d_climb)).ok()) return s;
-    const size_t qcap = n_items + 1024;
+    // unread slots of a ring <= its unclaimed items (one step per climbing
+    // leaf: n_items) + one claimed-but-unread ticket per resident warp
+    const size_t qcap = n_items + (size_t)a.sm_count * 64 + 1024;
     for (int lv = 0; lv < hpk::kRings; ++lv) {
       std::string nm = "q_slots" + std::to_string(lv);
       if (!(s = scratch(a, nm.c_str(), qcap, &q.slots[lv])).ok()) return s;
@@ -2361,6 +2401,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     q.tail[1] = d_q + 4;
     q.tail[2] = d_q + 5;
     q.active = reinterpret_cast<int*>(d_q + 6);
+    q.progress = d_q + 7;
     q.cap = qcap;
     q.hi_levels = 1LL << 17;
     q.r1_thr = -1;  // set below from the grid (one item per SM of backlog)
@@ -2438,7 +2479,9 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
       cudaMemcpy(ctr, q.head[0], sizeof ctr, cudaMemcpyDeviceToHost);
       char msg[256];
       std::snprintf(msg, sizeof msg,
-                    "watchdog: hill-climb work queue stalled (head %llu/%llu/%llu tail %llu/%llu/%llu active %d)",
+                    "%s (head %llu/%llu/%llu tail %llu/%llu/%llu active %d)",
+                    abort_flag == 2 ? "hill-climb work ring overwrote an unread item"
+                                    : "watchdog: hill-climb work queue made no progress for ~35 s",
                     ctr[0], ctr[1], ctr[2], ctr[3], ctr[4], ctr[5], (int)(ctr[6] & 0xffffffffu));
       return hph::Status{HP_INTERNAL, msg};
     }
@@ -2623,9 +2666,12 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   CK(cudaStreamSynchronize(st));
   out.simulated = counts[0];
   out.pruned = counts[1];
-  unsigned long long ops = 0;
-  CK(cudaMemcpy(&ops, d_ops, sizeof ops, cudaMemcpyDeviceToHost));
-  out.eval_fp64_ops = static_cast<double>(ops);
+  unsigned long long ops[4] = {0, 0, 0, 0};
+  CK(cudaMemcpy(ops, d_ops, sizeof ops, cudaMemcpyDeviceToHost));
+  out.eval_fp64_ops = static_cast<double>(ops[0]);
+  out.dev_simulated = static_cast<long long>(ops[1]);
+  out.dev_aborted = static_cast<long long>(ops[2]);
+  out.dev_screened = static_cast<long long>(ops[3]);
   if (a.time_evals) out.eval_ms = a.drain_events();
   a.d2h_bytes += sizeof(int) + sizeof counts + sizeof ops;
   out.has_best = best_leaf >= 0;
@@ -2869,8 +2915,8 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   int* d_next;
   if (!(s = scratch(a, "d_next", 4, &d_next)).ok()) return s;
   unsigned long long* d_ops;
-  if (!(s = scratch(a, "ops", 1, &d_ops)).ok()) return s;
-  CK(cudaMemsetAsync(d_ops, 0, sizeof(unsigned long long), st));
+  if (!(s = scratch(a, "ops", 4, &d_ops)).ok()) return s;
+  CK(cudaMemsetAsync(d_ops, 0, 4 * sizeof(unsigned long long), st));
   b.ops = d_ops;
 
   if (!have_bound) {
@@ -2913,14 +2959,17 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   CK(cudaGetLastError());
   int bt = -1;
   long long counts[3];
-  unsigned long long ops = 0;
+  unsigned long long ops[4] = {0, 0, 0, 0};
   CK(cudaMemcpyAsync(&bt, d_bt, sizeof bt, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(counts, d_counts, sizeof counts, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&ops, d_ops, sizeof ops, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ops, d_ops, sizeof ops, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (a.time_evals) out.eval_ms = a.drain_events();
   if (a.log.on && !(s = log_collect(a, b.log, tasks.size())).ok()) return s;
-  out.eval_fp64_ops = static_cast<double>(ops);
+  out.eval_fp64_ops = static_cast<double>(ops[0]);
+  out.dev_simulated = static_cast<long long>(ops[1]);
+  out.dev_aborted = static_cast<long long>(ops[2]);
+  out.dev_screened = static_cast<long long>(ops[3]);
   out.simulated = counts[0];
   out.pruned = counts[1] + counts[2];
   out.pruned_mem = counts[1];

@@ -232,13 +232,15 @@ def gather_results(res: abi.hp_result, world: int, group=None, device=None) -> L
 
 
 def search_sharded(docs: Dict[str, dict], rank: int, world: int, device: Optional[int] = None, group=None,
-                   shard_fn=None, probe_fn=None, log: bool = False) -> SearchOutcome:
+                   shard_fn=None, probe_fn=None, log: bool = False, flags: int = 0,
+                   mine: Optional[list] = None) -> SearchOutcome:
     """One shard per rank; default mode first all-reduces (MIN) the per-shard
     probe bounds (planner.cpp:640-651), then every rank searches its shard and
     the per-rank records are all-gathered in one collective; every rank
     applies the same exact reduction, so all ranks return the same plan.
     shard_fn/probe_fn replace the GPU engine (tests drive the CPU emulation
-    through the same reduction with gloo)."""
+    through the same reduction with gloo). `flags` adds HP_FLAG_* bits to
+    the shard call; `mine`, if given, receives this rank's own hp_result."""
     import torch
     import torch.distributed as dist
 
@@ -246,22 +248,26 @@ def search_sharded(docs: Dict[str, dict], rank: int, world: int, device: Optiona
     log_fn = None
     if shard_fn is None:
         eng = engine(device)
-        flags = abi.HP_FLAG_LOG if log else 0
-        shard_fn = lambda p, r, w, b: eng.search_shard(p, r, w, b, flags)  # noqa: E731
+        fl = flags | (abi.HP_FLAG_LOG if log else 0)
+        shard_fn = lambda p, r, w, b: eng.search_shard(p, r, w, b, fl)  # noqa: E731
         probe_fn = lambda p, r, w: eng.probe_shard(p, r, w)  # noqa: E731
         log_fn = eng.search_log
     bound = None
-    if problem.struct.planner.time_bound_pruning:
+    if problem.struct.planner.time_bound_pruning and world > 1:
         b = probe_fn(problem, rank, world)
         t = torch.tensor([b], dtype=torch.float64, device=f"cuda:{device}" if device is not None else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
         bound = float(t.item())
     res = shard_fn(problem, rank, world, bound)
-    red = reduce_results(problem, gather_results(res, world, group, device))
+    if mine is not None:
+        mine.append(res)
+    red = reduce_results(problem, gather_results(res, world, group, device)) if world > 1 else res
     entries = []
     if log and log_fn is not None:
-        parts = [None] * world
-        dist.all_gather_object(parts, log_fn(), group=group)  # cold path: variable-size log
+        parts = [log_fn()]
+        if world > 1:
+            parts = [None] * world
+            dist.all_gather_object(parts, log_fn(), group=group)  # cold path: variable-size log
         entries = merge_logs(parts)
     if not red.has_best:
         raise abi.InfeasibleError("no feasible plan found", infeasible_reasons(entries, red.tasks))

@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     for fn in decl:
         assert fn in syms, fn
         assert hasattr(l, fn)
-    assert l.hp_abi_version() == 1
+    assert l.hp_abi_version() == 2
 
 
 def test_struct_layout_matches_header(tmp_path):

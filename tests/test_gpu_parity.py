@@ -131,3 +131,24 @@ def test_bad_config_raises_config_error(engine):
     docs["model"]["num_heads"] = 7
     with pytest.raises(abi.ConfigError, match="divisible by num_heads"):
         planner.search(docs)
+
+
+def test_c4_c5_against_reference(engine):
+    """SURVEY §8d C4 (all six accelerator pairs, Llama-70B / 512 devices;
+    default mode over every pp with the search log, full mode on pp
+    {2..12}) and C5 (pp 3 exhaustive slices, 160 layers, 3 device types)
+    against the compiled reference's outcomes (tests/golden/gen_c4_c5.py)."""
+    import hashlib
+    from conftest import load_golden
+    cases = load_golden("c4_c5_cases.json")
+    assert sum(c["name"].startswith("C4:") for c in cases) == 12
+    assert any(c["name"].startswith("C5:") and c["status"] == 0 for c in cases)
+    for case in cases:
+        check_case(engine, case)
+        if "log" in case:
+            out = planner.search(case["docs"], log=True)
+            h = hashlib.sha256()
+            for e in out.log:
+                h.update(f"{e.candidate}\t{struct.pack('>d', e.time_s).hex()}\t{e.prune_reason}\n".encode())
+            assert len(out.log) == case["log"]["n"], case["name"]
+            assert h.hexdigest() == case["log"]["sha256"], case["name"]
