@@ -270,6 +270,56 @@ int hp_better_than(const hp_problem* problem, double time_a, const hp_plan* plan
 hp_status hp_evaluate_plans(hp_ctx* ctx, const hp_problem* problem, const hp_plan* plans,
                             int32_t n, double* iteration_time_s);
 
+/* Winner post-processing (planner.cpp:681-684): the full PlanEvaluation of
+ * evaluate_plan_unchecked(plan, ..., record_trace) (evaluate.cpp:78-107,
+ * evaluate.hpp:38-44), bit for bit. The simulation runs on the GPU (every
+ * node time); the trace sort, busy sums, in-flight counts, bubble ratios and
+ * peak memory follow on the host in the reference's order (sim.cpp:148-209). */
+
+/* TraceEvent, sim.hpp:34-42; kind: 0 F, 1 B, 2 SendF, 3 SendB */
+typedef struct hp_trace_event {
+  int32_t stage;
+  int32_t kind;
+  int32_t microbatch;
+  int32_t _pad;
+  double start_s;
+  double end_s;
+} hp_trace_event;
+
+/* Per stage: PlanCosts (evaluate.hpp:28-31) and SimResult's per-stage
+ * vectors (sim.hpp:44-53) after evaluate_plan_unchecked's DP-sync pass. */
+typedef struct hp_stage_eval {
+  double fwd_s;
+  double bwd_s;
+  double send_fwd_s;
+  double send_bwd_s;
+  double dp_sync_s;
+  double busy_s;            /* per_stage_busy_s (compute + DP sync) */
+  double compute_end_s;     /* per_stage_compute_end_s */
+  double bubble_ratio;      /* per_stage_bubble_ratio */
+  double peak_memory_bytes; /* peak_memory_bytes */
+  int32_t peak_in_flight;   /* peak_in_flight */
+  int32_t _pad;
+} hp_stage_eval;
+
+typedef struct hp_plan_eval {
+  double iteration_time_s;       /* sim.iteration_time_s (incl. DP sync) */
+  double pipeline_time_s;        /* flush time before gradient sync */
+  double aggregate_bubble_ratio;
+  int64_t micro_batches;
+  int64_t total_devices;         /* ParallelPlan::total_devices, types.cpp:71-76 */
+  int32_t n_stages;
+  int32_t _pad;
+  uint64_t n_trace;              /* trace events (4PM - 2M; written when trace != NULL) */
+} hp_plan_eval;
+
+/* stages: n_stages entries (caller-allocated). trace: NULL for no trace,
+ * else trace_cap >= 4*P*M - 2*M entries, sorted by (start, stage, kind,
+ * microbatch) like sim.cpp:162-167. Plan shape as hp_evaluate_plans. */
+hp_status hp_evaluate_plan_full(hp_ctx* ctx, const hp_problem* problem, const hp_plan* plan,
+                                hp_plan_eval* eval, hp_stage_eval* stages, hp_trace_event* trace,
+                                uint64_t trace_cap);
+
 #ifdef __cplusplus
 }
 #endif

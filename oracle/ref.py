@@ -32,6 +32,8 @@ def lib():
         l.ref_search_json.restype = ctypes.c_int
         l.ref_evaluate_json.argtypes = [cp, cp, cp, cp, ctypes.POINTER(ctypes.c_void_p)]
         l.ref_evaluate_json.restype = ctypes.c_int
+        l.ref_evaluate_trace_json.argtypes = [cp, cp, cp, cp, ctypes.POINTER(ctypes.c_void_p)]
+        l.ref_evaluate_trace_json.restype = ctypes.c_int
         l.ref_simulate.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
                                    ctypes.c_longlong, ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(ctypes.c_double)]
@@ -67,6 +69,15 @@ def evaluate(cfg: dict, plan: dict) -> dict:
     out = ctypes.c_void_p()
     enc = [json.dumps(cfg[k]).encode() for k in ("model", "cluster", "train")] + [json.dumps(plan).encode()]
     lib().ref_evaluate_json(*enc, ctypes.byref(out))
+    return _take(out)
+
+
+def evaluate_trace(cfg: dict, plan: dict) -> dict:
+    """evaluate_plan_unchecked(record_trace=true): every PlanEvaluation field
+    as bits plus the sorted trace."""
+    out = ctypes.c_void_p()
+    enc = [json.dumps(cfg[k]).encode() for k in ("model", "cluster", "train")] + [json.dumps(plan).encode()]
+    lib().ref_evaluate_trace_json(*enc, ctypes.byref(out))
     return _take(out)
 
 

@@ -135,6 +135,41 @@ int ref_evaluate_json(const char* model, const char* cluster, const char* train,
   return status;
 }
 
+// evaluate_plan_unchecked(record_trace = true) on one explicit plan: every
+// field of PlanEvaluation (evaluate.hpp:38-44) as bit patterns, plus the
+// sorted trace (sim.hpp:34-42) as [stage, kind, microbatch, start, end].
+int ref_evaluate_trace_json(const char* model, const char* cluster, const char* train,
+                            const char* plan, char** out) {
+  json result;
+  int status = 0;
+  try {
+    hetplan::ModelSpec m = hetplan::model_from_json(json::parse(model));
+    hetplan::ClusterSpec c = hetplan::cluster_from_json(json::parse(cluster));
+    hetplan::TrainConfig t = hetplan::train_from_json(json::parse(train));
+    hetplan::ParallelPlan p = hetplan::plan_from_json(json::parse(plan));
+    hetplan::PlanEvaluation e = hetplan::evaluate_plan_unchecked(p, m, c, t, true);
+    json ev = eval_json(e);
+    for (std::size_t i = 0; i < e.costs.times.size(); ++i) {
+      ev["stages"][i]["busy"] = hex_bits(e.sim.per_stage_busy_s[i]);
+      ev["stages"][i]["bubble"] = hex_bits(e.sim.per_stage_bubble_ratio[i]);
+    }
+    ev["micro_batches"] = e.micro_batches;
+    ev["total_devices"] = e.total_devices;
+    json tr = json::array();
+    for (const auto& x : e.sim.trace)
+      tr.push_back(json::array({x.stage, static_cast<int>(x.kind), x.microbatch, hex_bits(x.start_s),
+                                hex_bits(x.end_s)}));
+    ev["trace"] = std::move(tr);
+    result["eval"] = std::move(ev);
+  } catch (const std::exception& e) {
+    status = 3;
+    result["error"] = e.what();
+  }
+  result["status"] = status;
+  *out = dup_string(result.dump());
+  return status;
+}
+
 // simulate() (sim.cpp:63-195) on raw stage times: times is P x 4 doubles
 // (fwd, bwd, send_fwd, send_bwd). Writes the makespan and compute ends.
 int ref_simulate(int schedule_gpipe, const double* times, int P, long long M,

@@ -50,6 +50,9 @@ def lib():
     l.hp_search_log.argtypes = [C.c_void_p, P(abi.hp_log_entry), C.c_uint64, C.c_char_p, C.c_uint64,
                                 P(C.c_uint64), P(C.c_uint64)]
     l.hp_search_log.restype = C.c_int
+    l.hp_evaluate_plan_full.argtypes = [C.c_void_p, P(abi.hp_problem), P(abi.hp_plan), P(abi.hp_plan_eval),
+                                        P(abi.hp_stage_eval), P(abi.hp_trace_event), C.c_uint64]
+    l.hp_evaluate_plan_full.restype = C.c_int
     if l.hp_abi_version() != abi_version():
         raise NativeLibraryMissing("libhetplan_b200.so ABI version mismatch; rebuild")
     _lib = l
@@ -61,4 +64,4 @@ def abi_version() -> int:
 
 
 EXPORTED = ["hp_abi_version", "hp_create", "hp_destroy", "hp_last_error", "hp_validate", "hp_probe",
-            "hp_search", "hp_search_log", "hp_better_than", "hp_evaluate_plans"]
+            "hp_search", "hp_search_log", "hp_better_than", "hp_evaluate_plans", "hp_evaluate_plan_full"]

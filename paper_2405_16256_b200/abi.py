@@ -95,6 +95,24 @@ class hp_result(C.Structure):
                 ("device_aborted", C.c_int64), ("device_screened", C.c_int64), ("best_plan", hp_plan)]
 
 
+class hp_trace_event(C.Structure):
+    _fields_ = [("stage", C.c_int32), ("kind", C.c_int32), ("microbatch", C.c_int32), ("_pad", C.c_int32),
+                ("start_s", C.c_double), ("end_s", C.c_double)]
+
+
+class hp_stage_eval(C.Structure):
+    _fields_ = [("fwd_s", C.c_double), ("bwd_s", C.c_double), ("send_fwd_s", C.c_double),
+                ("send_bwd_s", C.c_double), ("dp_sync_s", C.c_double), ("busy_s", C.c_double),
+                ("compute_end_s", C.c_double), ("bubble_ratio", C.c_double), ("peak_memory_bytes", C.c_double),
+                ("peak_in_flight", C.c_int32), ("_pad", C.c_int32)]
+
+
+class hp_plan_eval(C.Structure):
+    _fields_ = [("iteration_time_s", C.c_double), ("pipeline_time_s", C.c_double),
+                ("aggregate_bubble_ratio", C.c_double), ("micro_batches", C.c_int64), ("total_devices", C.c_int64),
+                ("n_stages", C.c_int32), ("_pad", C.c_int32), ("n_trace", C.c_uint64)]
+
+
 class hp_log_entry(C.Structure):
     _fields_ = [("candidate", C.c_uint64), ("reason", C.c_uint64), ("time_s", C.c_double),
                 ("task", C.c_int32), ("leaf", C.c_int32)]

@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "--fmad=false", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
           "-I" + os.path.join(HERE, "..", "include")]
-SOURCES = ["hp_kernels.cu", "hp_host.cpp", "hp_log.cpp", "hp_capi.cpp"]
+SOURCES = ["hp_kernels.cu", "hp_host.cpp", "hp_log.cpp", "hp_eval.cpp", "hp_capi.cpp"]
 
 
 def _newest_dep_mtime() -> float:

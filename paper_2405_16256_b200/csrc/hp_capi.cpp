@@ -10,6 +10,7 @@
 
 #include "../../include/hetplan_b200.h"
 #include "hp_device.hpp"
+#include "hp_eval.hpp"
 #include "hp_host.hpp"
 #include "hp_log.hpp"
 
@@ -287,6 +288,20 @@ hp_status hp_evaluate_plans(hp_ctx* ctx, const hp_problem* problem, const hp_pla
     if (!c.ok()) return fail(ctx, c);
   }
   s = hpd::evaluate_plans(ctx->arena, p, plans, n, iteration_time_s);
+  return s.ok() ? HP_OK : fail(ctx, s);
+}
+
+hp_status hp_evaluate_plan_full(hp_ctx* ctx, const hp_problem* problem, const hp_plan* plan, hp_plan_eval* eval,
+                                hp_stage_eval* stages, hp_trace_event* trace, uint64_t trace_cap) {
+  if (!ctx) return HP_INTERNAL;
+  cudaSetDevice(ctx->arena.device);
+  hph::Problem p;
+  hph::Status s = hph::load_problem(problem, p);
+  if (!s.ok()) return fail(ctx, s);
+  if (!plan || !eval || !stages) return fail(ctx, HP_BAD_CONFIG, "hp_evaluate_plan_full: null argument");
+  s = check_plan_shape(p, *plan);
+  if (!s.ok()) return fail(ctx, s);
+  s = hpe::evaluate_plan_full(ctx->arena, p, *plan, eval, stages, trace, trace_cap);
   return s.ok() ? HP_OK : fail(ctx, s);
 }
 

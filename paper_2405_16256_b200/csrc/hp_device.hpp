@@ -156,6 +156,17 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
 hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<int>& my_tasks,
                            bool have_bound, double bound, bool probe_only, SearchOut& out);
 
+// Every node time of one explicit plan (winner post-processing): dur = per
+// stage (f, b, sf, sb, dps); nodes = 8 arrays of P*M doubles (F start/end,
+// B start/end, SendF start/end, SendB start/end at [stage * M + microbatch]);
+// fin = per stage (final stage_free, forward channel end, backward channel end).
+struct PlanNodes {
+  int P = 0;
+  long long M = 0;
+  std::vector<double> dur, nodes, fin;
+};
+hph::Status plan_node_times(Arena& a, const hph::Problem& p, const hp_plan& plan, PlanNodes& out);
+
 // Batched evaluate_plan_unchecked(...).sim.iteration_time_s of explicit plans.
 hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans, int n,
                            double* out_times);

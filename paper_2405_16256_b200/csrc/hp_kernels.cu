@@ -847,14 +847,13 @@ __global__ void __launch_bounds__(256) k_eval(Bufs b, const Work* items, const i
 // a full ring advances one ring's worth of items per step. Ring-0 items run
 // the lowest-latency evaluator for their P (K = 4 up to P = 128: fewer
 // stages per lane, a shorter level) and only warps 0-3 of each block serve
-// ring 0 (one per SM sub-partition). A warp claims a ticket only below the
-// ring's tail (CAS on head), so every claimed ticket has been pushed and its
-// slot is read right after the producer's write lands: no warp holds a
-// ticket across items. The slots a ring can have unread are then its
-// unclaimed items plus one per resident warp, both bounded by the ring
-// capacity (one step per climbing leaf, plus the resident warps), so the
-// producer never laps an unread slot; a consumer that finds its slot's
-// sequence number past its ticket reports the overwrite instead of hanging.
+// ring 0 (one per SM sub-partition). Each warp holds at most one ticket per
+// ring and serves a held ticket as soon as it is filled (pop_item), so a
+// filled slot stays unread for at most one item's run; the ring capacity
+// (one step per climbing leaf plus the resident warps, + slack) bounds the
+// unread slots otherwise. A consumer that finds its slot's sequence number
+// past its ticket (lapped) aborts the search with an error instead of
+// hanging.
 constexpr int kRings = 3;
 
 struct AsyncQ {
@@ -1473,18 +1472,13 @@ __global__ void k_async_seed(Bufs b, AsyncQ q, const int* ids, int n) {
   advance_leaf(b, q, li, lane, false);
 }
 
-// Reads the item of a claimed ticket (below the tail: the producer has
-// bumped the tail and is writing or has written the slot). Returns false
-// when the slot was lapped (its sequence number is past the ticket), which
-// the ring sizing rules out; the caller aborts the search loudly.
-__device__ __forceinline__ bool read_slot(const AsyncQ& q, int lv, unsigned long long h, Work& w) {
+// Slot state of a claimed ticket h: 1 filled (item read into w), 0 not yet
+// filled, -1 lapped (the slot's sequence number is past the ticket: the
+// producer of ticket h + cap overwrote the unread item).
+__device__ __forceinline__ int try_slot(const AsyncQ& q, int lv, unsigned long long h, Work& w) {
   const unsigned long long k = h % q.cap;
-  for (;;) {
-    const unsigned long long s = *(volatile unsigned long long*)(q.seq[lv] + k);
-    if (s == h + 1) break;
-    if (s > h + 1) return false;
-    __nanosleep(20);
-  }
+  const unsigned long long sq = *(volatile unsigned long long*)(q.seq[lv] + k);
+  if (sq != h + 1) return sq > h + 1 ? -1 : 0;
   __threadfence();
   const Work* sl = q.slots[lv] + k;
   w.leaf = __ldcg(&sl->leaf);
@@ -1492,40 +1486,59 @@ __device__ __forceinline__ bool read_slot(const AsyncQ& q, int lv, unsigned long
   w.first = __ldcg(&sl->first);
   w.n = __ldcg(&sl->n);
   w.out = __ldcg(&sl->out);
-  return true;
+  return 1;
 }
 
-// Claims the next ticket of ring lv if one is below the tail.
-__device__ __forceinline__ bool claim(const AsyncQ& q, int lv, bool lead, unsigned long long& ticket) {
-  unsigned long long hd = *(volatile unsigned long long*)q.head[lv];
-  for (;;) {
-    const unsigned long long tl = *(volatile unsigned long long*)q.tail[lv];
-    // (r1_thr > 0: a non-lead warp takes a long-climber item only from a
-    // backlog above r1_thr, so a thin ring 1 runs one item per sub-partition)
-    if (!(tl > hd && (lv != 1 || lead || tl - hd > (unsigned long long)q.r1_thr))) return false;
-    const unsigned long long old = atomicCAS(q.head[lv], hd, hd + 1);
-    if (old == hd) {
-      ticket = hd;
-      return true;
-    }
-    hd = old;
-  }
-}
-
-// Lane 0: next item for this warp (see AsyncQ), highest-priority ring first.
-// Returns false when the warp should exit (no leaf climbing, or abort).
-__device__ bool pop_item(const AsyncQ& q, Work& w, int lv0, bool lead) {
+// Lane 0: next item for this warp (see AsyncQ). Tickets are claimed with
+// atomicAdd only when the ring shows unclaimed items (a CAS claim caps the
+// claim rate at one per L2 round trip, 4x slower on C3); racing claims can
+// pass the tail, and such a ticket is held until a later push fills it while
+// the warp serves other rings. A held ticket that is filled is served before
+// anything else, so it stays unread for at most the one item in progress
+// when it was filled. Returns false when the warp should exit (no leaf
+// climbing, or abort).
+__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int lv0, bool lead) {
   unsigned ns = 32;
   long long t0 = clock64();
   unsigned long long seen = *(volatile unsigned long long*)q.progress;
   for (;;) {
+    // 1) a held ticket that has been filled meanwhile
     for (int lv = lv0; lv < kRings; ++lv) {
-      unsigned long long tk;
-      if (claim(q, lv, lead, tk)) {
-        if (read_slot(q, lv, tk, w)) return true;
+      if (tk[lv] < 0) continue;
+      const int r = try_slot(q, lv, (unsigned long long)tk[lv], w);
+      if (r < 0) {
         atomicExch(q.abort, 2);
         return false;
       }
+      if (r > 0) {
+        tk[lv] = -1;
+        return true;
+      }
+    }
+    // 2) new claims, highest-priority ring first; a claimed higher-priority
+    // ticket that is being filled (the producer bumps the tail before it
+    // writes the slot) is waited for rather than a lower ring started
+    bool held = false;
+    for (int lv = lv0; lv < kRings && !held; ++lv) {
+      const unsigned long long tl = *(volatile unsigned long long*)q.tail[lv];
+      const unsigned long long hd = *(volatile unsigned long long*)q.head[lv];
+      // (r1_thr > 0: a non-lead warp takes a long-climber item only from a
+      // backlog above r1_thr, so a thin ring 1 runs one item per sub-partition)
+      if (tk[lv] < 0 && tl > hd && (lv != 1 || lead || tl - hd > (unsigned long long)q.r1_thr)) {
+        tk[lv] = (long long)atomicAdd(q.head[lv], 1ULL);
+        const int r = try_slot(q, lv, (unsigned long long)tk[lv], w);
+        if (r < 0) {
+          atomicExch(q.abort, 2);
+          return false;
+        }
+        if (r > 0) {
+          tk[lv] = -1;
+          return true;
+        }
+      }
+      // (a ticket past the tail — claimed in a race — waits for a future
+      // push and must not hold back the lower rings)
+      held = tk[lv] >= 0 && (unsigned long long)tk[lv] < *(volatile unsigned long long*)q.tail[lv];
     }
     const int act = *(volatile int*)q.active;
     if (act == 0 || *(volatile int*)q.abort) return false;
@@ -1540,7 +1553,7 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, int lv0, bool lead) {
       atomicExch(q.abort, 1);
       return false;
     }
-    __nanosleep(ns);
+    __nanosleep(held ? 32 : ns);
     if (ns < 256) ns <<= 1;
   }
 }
@@ -1566,6 +1579,7 @@ __device__ __noinline__ void eval_item_call(const Bufs& b, const Work& w, int la
 
 __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ q) {
   const int lane = threadIdx.x & 31;
+  long long tk[kRings] = {-1, -1, -1};
   if (q.crit_sms > 0 && (int)blockIdx.x < q.crit_sms && (threadIdx.x >> 5) >= 4) return;
   for (;;) {
     int quit = 0, cls = 0;
@@ -1577,7 +1591,7 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
       const int wib = threadIdx.x >> 5;
       int lv0 = wib < 4 || !q.lead ? 0 : 1;
       if (q.crit_sms > 0) lv0 = (int)blockIdx.x < q.crit_sms ? 0 : 1;
-      quit = pop_item(q, w, lv0, wib < 4) ? 0 : 1;
+      quit = pop_item(q, w, tk, lv0, wib < 4) ? 0 : 1;
       if (!quit) cls = w.out > 0 ? w.out - 1 : leaf_class(b.leaves[w.leaf]);
     }
     quit = __shfl_sync(0xffffffffu, quit, 0);
@@ -2080,6 +2094,100 @@ __global__ void k_final_tasks(Bufs b, const TaskRes* res, const TaskDev* tasks, 
   }
 }
 
+// ------------------------------------------------------------------ plan trace
+//
+// Winner post-processing (planner.cpp:681-684): every node time of ONE
+// explicit plan, for the trace, busy times and in-flight counts of
+// evaluate_plan_unchecked(record_trace = true) (evaluate.cpp:78-107,
+// sim.cpp:63-195). One block, thread i = stage i; level-synchronous like the
+// search evaluators (the unit-time ASAP order of hp_core.cuh stage_level,
+// whose doubles are the reference's), with the neighbours' previous-level
+// channel state exchanged through shared memory and every op's start / end
+// and its send's start / end recorded. nodes: 8 arrays of P*M doubles,
+// [F start, F end, B start, B end, SendF start, SendF end, SendB start,
+// SendB end] at [stage * M + microbatch]. dur: per stage f, b, sf, sb, dps.
+// fin: per stage final stage_free, forward / backward channel ends.
+__global__ void __launch_bounds__(256) k_plan_trace(Bufs b, double* dur, double* nodes, double* fin) {
+  __shared__ double s_chf[HP_MAX_STAGES], s_chb[HP_MAX_STAGES];
+  __shared__ int s_nf[HP_MAX_STAGES], s_nb[HP_MAX_STAGES];
+  const Leaf lf = b.leaves[0];
+  const int P = lf.P, M = lf.M;
+  const bool gpipe = lf.sched == 0;
+  const int i = threadIdx.x;
+  const size_t PM = (size_t)P * M;
+  StageDur d{0.0, 0.0, 0.0, 0.0, 0.0};
+  if (i < P) {
+    stage_setup(c_consts, lf, b.lg + lf.lg_off, b.layouts + lf.layout_off, b.hop + lf.B_idx * c_consts.n_links, i,
+                b.uni[lf.split_off + i], d);
+    dur[5 * i + 0] = d.f;
+    dur[5 * i + 1] = d.b;
+    dur[5 * i + 2] = d.sf;
+    dur[5 * i + 3] = d.sb;
+    dur[5 * i + 4] = d.dps;
+  }
+  StageState st;
+  stage_init(st);
+  const int wb = gpipe ? M : min(P - i, M);
+  double* row = nodes + (size_t)i * M;
+  for (;;) {
+    if (i < P) {
+      s_chf[i] = st.chf;
+      s_nf[i] = st.nf;
+      s_chb[i] = st.chb;
+      s_nb[i] = st.nb;
+    }
+    __syncthreads();
+    const double lchf = i > 0 && i < P ? s_chf[i - 1] : 0.0;
+    const int lnf = i > 0 && i < P ? s_nf[i - 1] : 0;
+    const double rchb = i + 1 < P ? s_chb[i + 1] : 0.0;
+    const int rnb = i + 1 < P ? s_nb[i + 1] : 0;
+    const bool done = i >= P || stage_done(st, M);
+    if (__syncthreads_and(done)) break;
+    if (done) continue;
+    // stage_level (hp_core.cuh) with every node recorded
+    bool want_f;
+    if (gpipe) want_f = st.nf < M;
+    else want_f = st.nf < wb || (st.nf < M && st.nb > st.nf - wb);
+    if (!want_f && st.nb >= M) continue;
+    if (want_f) {
+      if (i > 0 && !(lnf > st.nf)) continue;            // ready(), sim.cpp:102
+      const double start = dmax(st.free_t, i > 0 ? lchf : 0.0);
+      const double end = start + d.f;
+      st.free_t = end;
+      row[st.nf] = start;
+      row[PM + st.nf] = end;
+      if (i < P - 1) {                                  // sim.cpp:125-134
+        const double ss = dmax(end, st.chf);
+        const double e = ss + d.sf;
+        st.chf = e;
+        row[4 * PM + st.nf] = ss;
+        row[5 * PM + st.nf] = e;
+      }
+      st.nf++;
+    } else {
+      if (i < P - 1 && !(rnb > st.nb)) continue;        // ready(), sim.cpp:103
+      const double start = dmax(st.free_t, i < P - 1 ? rchb : 0.0);
+      const double end = start + d.b;
+      st.free_t = end;
+      row[2 * PM + st.nb] = start;
+      row[3 * PM + st.nb] = end;
+      if (i > 0) {                                      // sim.cpp:135-145
+        const double ss = dmax(end, st.chb);
+        const double e = ss + d.sb;
+        st.chb = e;
+        row[6 * PM + st.nb] = ss;
+        row[7 * PM + st.nb] = e;
+      }
+      st.nb++;
+    }
+  }
+  if (i < P) {
+    fin[3 * i + 0] = st.free_t;
+    fin[3 * i + 1] = st.chf;
+    fin[3 * i + 2] = st.chb;
+  }
+}
+
 }  // namespace hpk
 
 // ====================================================================== host
@@ -2381,9 +2489,9 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     if (!(s = scratch(a, "q_pending", nL, &q.pending)).ok()) return s;
     int* d_climb;
     if (!(s = upload(a, "climb_ids", climb, &d_climb)).ok()) return s;
-    // unread slots of a ring <= its unclaimed items (one step per climbing
-    // leaf: n_items) + one claimed-but-unread ticket per resident warp
-    const size_t qcap = n_items + (size_t)a.sm_count * 64 + 1024;
+    // unread slots of a ring: its unclaimed items (one step per climbing
+    // leaf: <= n_items) + one held ticket per resident warp, + slack
+    const size_t qcap = 2 * n_items + (size_t)a.sm_count * 64 + 65536;
     for (int lv = 0; lv < hpk::kRings; ++lv) {
       std::string nm = "q_slots" + std::to_string(lv);
       if (!(s = scratch(a, nm.c_str(), qcap, &q.slots[lv])).ok()) return s;
@@ -2773,6 +2881,79 @@ hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans
   CK(cudaMemcpyAsync(t.data(), b.tseed, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int k = 0; k < n; ++k) out_times[k] = t[2 * (size_t)k];
+  return hph::Status{};
+}
+
+
+// Node times of one explicit plan on the GPU (k_plan_trace), for the winner
+// post-processing of hp_evaluate_plan_full (hp_eval.cpp).
+hph::Status plan_node_times(Arena& a, const hph::Problem& p, const hp_plan& pl, PlanNodes& out) {
+  cudaStream_t st = a.stream;
+  Consts c;
+  hph::fill_consts(p, c);
+  c.n_B = 1;
+  CK(cudaMemcpyToSymbolAsync(hpk::c_consts, &c, sizeof c, 0, cudaMemcpyHostToDevice, st));
+  const int P = pl.n_stages;
+  const long long M = pl.micro_batches_per_dp_replica;
+  const int64_t B = pl.micro_batch_size > 0 ? pl.micro_batch_size : p.train.micro_batch_size;
+  std::vector<Leaf> leaves(1);
+  Leaf& lf = leaves[0];
+  lf.task = -1;
+  lf.P = P;
+  lf.M = static_cast<int>(M);
+  lf.dp = pl.stages[0].dp_degree;
+  lf.B = B;
+  lf.B_idx = 0;
+  lf.layout_off = 0;
+  lf.split_off = 0;
+  lf.lg_off = 0;
+  lf.mode = 3;
+  lf.sched = pl.schedule;
+  std::vector<LeafGroup> lgs;
+  std::vector<uint8_t> layouts;
+  std::vector<int> counts;
+  std::vector<double> hop(p.links.size());
+  for (size_t l = 0; l < p.links.size(); ++l) hop[l] = hph::hop_time(p, (int)l, B);
+  for (int i = 0; i < P; ++i) {
+    const hp_stage& s = pl.stages[i];
+    layouts.push_back(static_cast<uint8_t>(i));
+    counts.push_back(s.layer_end - s.layer_begin);
+    lgs.push_back(hph::leaf_group(p, s.group, s.tp_degree, B, s.dp_degree, s.nodes_used));
+  }
+  hpk::Bufs b{};
+  hph::Status s;
+  Leaf* d_leaves;
+  LeafGroup* d_lg;
+  uint8_t* d_layouts;
+  double* d_hop;
+  int* d_counts;
+  if (!(s = upload(a, "t_leaves", leaves, &d_leaves)).ok()) return s;
+  if (!(s = upload(a, "t_lg", lgs, &d_lg)).ok()) return s;
+  if (!(s = upload(a, "t_layouts", layouts, &d_layouts)).ok()) return s;
+  if (!(s = upload(a, "t_hop", hop, &d_hop)).ok()) return s;
+  if (!(s = upload(a, "t_counts", counts, &d_counts)).ok()) return s;
+  b.leaves = d_leaves;
+  b.lg = d_lg;
+  b.layouts = d_layouts;
+  b.hop = d_hop;
+  b.uni = d_counts;
+  const size_t PM = (size_t)P * (size_t)M;
+  double *d_dur, *d_nodes, *d_fin;
+  if (!(s = scratch(a, "t_dur", 5 * (size_t)P, &d_dur)).ok()) return s;
+  if (!(s = scratch(a, "t_nodes", 8 * PM, &d_nodes)).ok()) return s;
+  if (!(s = scratch(a, "t_fin", 3 * (size_t)P, &d_fin)).ok()) return s;
+  const int threads = ((P + 31) / 32) * 32;
+  hpk::k_plan_trace<<<1, threads, 0, st>>>(b, d_dur, d_nodes, d_fin);
+  CK(cudaGetLastError());
+  out.P = P;
+  out.M = M;
+  out.dur.resize(5 * (size_t)P);
+  out.nodes.resize(8 * PM);
+  out.fin.resize(3 * (size_t)P);
+  CK(cudaMemcpyAsync(out.dur.data(), d_dur, sizeof(double) * out.dur.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out.nodes.data(), d_nodes, sizeof(double) * out.nodes.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out.fin.data(), d_fin, sizeof(double) * out.fin.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   return hph::Status{};
 }
 

@@ -2,6 +2,7 @@
 
     search(docs, jobs=1, log=False) -> SearchOutcome   (planner.hpp:115-116)
     evaluate_plans(docs, plans) -> [iteration_time_s]  (evaluate.hpp:56-58, batched)
+    evaluate_plan(docs, plan, trace) -> PlanEvaluation  (evaluate.hpp:56-58, record_trace)
 
 `docs` are the reference's own JSON documents {"model","cluster","train",
 "planner"} (json_io.cpp:83-219). Errors raise the reference's exception kinds
@@ -119,6 +120,28 @@ class Engine:
         return list(out)[:n]
 
 
+    def evaluate_plan_full(self, problem: abi.Problem, plan: abi.hp_plan, trace: bool = True) -> "PlanEvaluation":
+        ev = abi.hp_plan_eval()
+        st = (abi.hp_stage_eval * max(1, plan.n_stages))()
+        n_tr = 4 * plan.n_stages * plan.micro_batches_per_dp_replica - 2 * plan.micro_batches_per_dp_replica
+        tr = (abi.hp_trace_event * max(1, n_tr))() if trace else None
+        rc = self._lib.hp_evaluate_plan_full(self._ctx, problem.ptr(), C.byref(plan), C.byref(ev), st, tr,
+                                             n_tr if trace else 0)
+        if rc != abi.HP_OK:
+            self._raise(rc, "hp_evaluate_plan_full")
+        return PlanEvaluation(ev, [st[i] for i in range(plan.n_stages)],
+                              [tr[i] for i in range(ev.n_trace)] if trace else [])
+
+
+@dataclass
+class PlanEvaluation:
+    """PlanEvaluation of evaluate.hpp:38-44 (with SimResult, sim.hpp:44-53):
+    scalars in `eval`, per-stage vectors in `stages`, the sorted trace."""
+    eval: abi.hp_plan_eval
+    stages: List[abi.hp_stage_eval]
+    trace: List[abi.hp_trace_event]
+
+
 _engines: Dict[int, Engine] = {}
 
 
@@ -180,6 +203,13 @@ def search(docs: Dict[str, dict], jobs: int = 1, device: int = 0, log: bool = Fa
     out = _outcome(problem, res)
     out.log = entries
     return out
+
+
+def evaluate_plan(docs: Dict[str, dict], plan: dict, trace: bool = True, device: int = 0) -> PlanEvaluation:
+    """evaluate_plan_unchecked(plan, ..., record_trace) (evaluate.hpp:56-58):
+    the winner post-processing of search() (planner.cpp:681-684)."""
+    problem = abi.Problem(docs)
+    return engine(device).evaluate_plan_full(problem, problem.plan_from_doc(plan), trace)
 
 
 def evaluate_plans(docs: Dict[str, dict], plans: List[dict], device: int = 0) -> List[float]:

@@ -40,7 +40,8 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layout_matches_header(tmp_path):
     structs = ["hp_model", "hp_group", "hp_link", "hp_cluster", "hp_train", "hp_planner", "hp_problem",
-               "hp_stage", "hp_plan", "hp_search_opts", "hp_result", "hp_log_entry"]
+               "hp_stage", "hp_plan", "hp_search_opts", "hp_result", "hp_log_entry", "hp_trace_event",
+               "hp_stage_eval", "hp_plan_eval"]
     src = tmp_path / "layout.c"
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for s in structs:
