@@ -270,6 +270,28 @@ int hp_better_than(const hp_problem* problem, double time_a, const hp_plan* plan
 hp_status hp_evaluate_plans(hp_ctx* ctx, const hp_problem* problem, const hp_plan* plans,
                             int32_t n, double* iteration_time_s);
 
+/* Multi-GPU search inside one process (the reference's `jobs` thread pool,
+ * planner.cpp:612-664, becomes one host thread per GPU): hp_multi_create
+ * binds one context per listed CUDA device and one NCCL communicator per
+ * device (ncclCommInitAll; NCCL is loaded at run time). hp_search_multi
+ * runs shard r on device r; default mode all-reduces (MIN) the shards' probe
+ * minima into the global bound (planner.cpp:640-651), and the fixed-size
+ * per-shard records are all-gathered (one NCCL collective each) and reduced
+ * with better_than (planner.cpp:656-664). `result` is the reduced record
+ * (device_ms = the slowest shard); per_device (optional) receives each
+ * shard's record. Equal, bit for bit, to hp_search on one device.
+ * hp_multi_search_log merges the shards' logs (HP_FLAG_LOG) in the
+ * reference's order, with hp_search_log's buffer protocol. */
+typedef struct hp_multi hp_multi;
+int hp_device_count(void); /* visible CUDA devices (0 without a GPU) */
+hp_status hp_multi_create(hp_multi** out, const int32_t* devices, int32_t n_devices);
+void hp_multi_destroy(hp_multi* multi);
+const char* hp_multi_last_error(const hp_multi* multi);
+hp_status hp_search_multi(hp_multi* multi, const hp_problem* problem, int32_t flags, hp_result* result,
+                          hp_result* per_device);
+hp_status hp_multi_search_log(hp_multi* multi, hp_log_entry* entries, uint64_t entry_cap, char* text,
+                              uint64_t text_cap, uint64_t* n_entries, uint64_t* text_bytes);
+
 /* Winner post-processing (planner.cpp:681-684): the full PlanEvaluation of
  * evaluate_plan_unchecked(plan, ..., record_trace) (evaluate.cpp:78-107,
  * evaluate.hpp:38-44), bit for bit. The simulation runs on the GPU (every

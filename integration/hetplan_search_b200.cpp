@@ -6,9 +6,10 @@
 // (planner.hpp:115-116; reference body planner.cpp:579-685) by flattening the
 // specs into the C ABI of include/hetplan_b200.h, running hp_search on the
 // GPU and rebuilding SearchOutcome: the winner plan (make_plan,
-// planner.cpp:553-575), its full evaluation with trace (planner.cpp:681-684,
-// the reference's own evaluate_plan_unchecked — cold, once per search), the
-// candidate counts and the search log (hp_search_log). Errors keep the
+// planner.cpp:553-575), its full evaluation with trace (planner.cpp:681-684:
+// hp_evaluate_plan_full), the candidate counts and the search log
+// (hp_search_log). `jobs` (the reference's worker threads) selects how many
+// of the box's GPUs search in parallel (hp_search_multi, NCCL between them). Errors keep the
 // reference's exception types: ConfigError for spec/planner problems,
 // InfeasibleError with the first 200 distinct "candidate -> reason" lines
 // (planner.cpp:666-678).
@@ -17,8 +18,10 @@
 // INTEGRATION.md); integration/Makefile does exactly that against the
 // unmodified reference sources to run the reference's callers on the GPU.
 //
-// Environment: HETPLAN_B200_DEVICE (CUDA device, default 0);
+// Environment: HETPLAN_B200_DEVICE (CUDA device of single-GPU searches,
+// default 0); HETPLAN_B200_DEVICES="0,1,..." (the GPUs, overriding jobs);
 // HETPLAN_B200_LOG=0 skips the search log for callers that never read it.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -133,10 +136,13 @@ ParallelPlan unflatten(const hp_plan& p, const ClusterSpec& c) {
   return plan;
 }
 
-// One engine context per process (the reference's search is re-entrant per
-// call; calls here are serialised on the context).
+// Engine contexts per process (the reference's search is re-entrant per
+// call; calls here are serialised): one single-GPU context, and one
+// multi-GPU group per device list.
 std::mutex g_mu;
 hp_ctx* g_ctx = nullptr;
+hp_multi* g_multi = nullptr;
+std::vector<int32_t> g_multi_devs;
 
 hp_ctx* context() {
   if (!g_ctx) {
@@ -147,18 +153,91 @@ hp_ctx* context() {
   return g_ctx;
 }
 
-[[noreturn]] void raise(hp_ctx* ctx, hp_status st) {
-  std::string msg = hp_last_error(ctx);
+[[noreturn]] void raise_msg(hp_status st, const std::string& msg) {
   if (st == HP_BAD_CONFIG) throw ConfigError(msg);
   if (st == HP_INFEASIBLE) throw InfeasibleError(msg);
   throw std::runtime_error("hetplan_b200: " + msg);
+}
+
+[[noreturn]] void raise(hp_ctx* ctx, hp_status st) { raise_msg(st, hp_last_error(ctx)); }
+
+// GPUs for a search: HETPLAN_B200_DEVICES="0,1,..." if set, else `jobs`
+// ("parallel search workers", tools/main.cpp:43) capped at the visible GPUs.
+std::vector<int32_t> devices_for(int jobs) {
+  std::vector<int32_t> d;
+  if (const char* e = std::getenv("HETPLAN_B200_DEVICES")) {
+    std::string s(e);
+    size_t pos = 0;
+    while (pos < s.size()) {
+      size_t q = s.find(',', pos);
+      if (q == std::string::npos) q = s.size();
+      if (q > pos) d.push_back(std::atoi(s.substr(pos, q - pos).c_str()));
+      pos = q + 1;
+    }
+    return d;
+  }
+  const int n = std::min(std::max(jobs, 1), std::max(hp_device_count(), 1));
+  for (int i = 0; i < n; ++i) d.push_back(i);
+  return d;
+}
+
+hp_multi* multi(const std::vector<int32_t>& devs) {
+  if (!g_multi || g_multi_devs != devs) {
+    if (g_multi) hp_multi_destroy(g_multi);
+    g_multi = nullptr;
+    hp_multi* m = nullptr;
+    hp_status st = hp_multi_create(&m, devs.data(), static_cast<int32_t>(devs.size()));
+    if (st != HP_OK) {
+      std::string msg = hp_multi_last_error(m);
+      hp_multi_destroy(m);
+      raise_msg(st, msg);
+    }
+    g_multi = m;
+    g_multi_devs = devs;
+  }
+  return g_multi;
+}
+
+// The winner's PlanEvaluation (planner.cpp:681-684) from
+// hp_evaluate_plan_full: GPU simulation with every node time, trace and
+// per-stage vectors (evaluate.hpp:38-44, sim.hpp:34-53).
+PlanEvaluation evaluate_winner(hp_ctx* ctx, const hp_problem& prob, const hp_plan& plan) {
+  const int P = plan.n_stages;
+  const uint64_t cap = 4ULL * P * plan.micro_batches_per_dp_replica - 2ULL * plan.micro_batches_per_dp_replica;
+  hp_plan_eval ev{};
+  std::vector<hp_stage_eval> st(P);
+  std::vector<hp_trace_event> tr(cap);
+  hp_status s = hp_evaluate_plan_full(ctx, &prob, &plan, &ev, st.data(), tr.data(), cap);
+  if (s != HP_OK) raise(ctx, s);
+  PlanEvaluation out;
+  out.pipeline_time_s = ev.pipeline_time_s;
+  out.micro_batches = ev.micro_batches;
+  out.total_devices = ev.total_devices;
+  out.costs.times.resize(P);
+  out.costs.dp_sync_s.resize(P);
+  SimResult& sim = out.sim;
+  sim.iteration_time_s = ev.iteration_time_s;
+  sim.aggregate_bubble_ratio = ev.aggregate_bubble_ratio;
+  for (int i = 0; i < P; ++i) {
+    out.costs.times[i] = {st[i].fwd_s, st[i].bwd_s, st[i].send_fwd_s, st[i].send_bwd_s};
+    out.costs.dp_sync_s[i] = st[i].dp_sync_s;
+    sim.per_stage_busy_s.push_back(st[i].busy_s);
+    sim.per_stage_compute_end_s.push_back(st[i].compute_end_s);
+    sim.per_stage_bubble_ratio.push_back(st[i].bubble_ratio);
+    sim.peak_in_flight.push_back(st[i].peak_in_flight);
+    sim.peak_memory_bytes.push_back(st[i].peak_memory_bytes);
+  }
+  sim.trace.reserve(ev.n_trace);
+  for (uint64_t k = 0; k < ev.n_trace; ++k)
+    sim.trace.push_back({tr[k].stage, static_cast<EventKind>(tr[k].kind), tr[k].microbatch, tr[k].start_s,
+                         tr[k].end_s});
+  return out;
 }
 
 }  // namespace
 
 SearchOutcome search(const ModelSpec& model, const ClusterSpec& cluster, const TrainConfig& cfg,
                      const PlannerConfig& pcfg, int jobs) {
-  (void)jobs;  // the GPU replaces the thread pool; results never depended on it
   Flat f;
   flatten(model, cluster, cfg, pcfg, f);
   const char* lg = std::getenv("HETPLAN_B200_LOG");
@@ -166,25 +245,38 @@ SearchOutcome search(const ModelSpec& model, const ClusterSpec& cluster, const T
 
   std::lock_guard<std::mutex> lock(g_mu);
   hp_ctx* ctx = context();
-  hp_search_opts opts{0, 1, 0, want_log ? HP_FLAG_LOG : 0, 0.0};
+  // jobs -> GPUs of this box (planner.cpp:612-664's thread pool); the result
+  // is the same for any count, like the reference's for any jobs
+  const std::vector<int32_t> devs = devices_for(jobs);
+  hp_multi* mg = devs.size() > 1 ? multi(devs) : nullptr;
+  auto run = [&](int32_t flags, hp_result& res) {
+    if (mg) {
+      hp_status st = hp_search_multi(mg, &f.prob, flags, &res, nullptr);
+      if (st != HP_OK) raise_msg(st, hp_multi_last_error(mg));
+      return;
+    }
+    hp_search_opts opts{0, 1, 0, flags, 0.0};
+    hp_status st = hp_search(ctx, &f.prob, &opts, &res);
+    if (st != HP_OK) raise(ctx, st);
+  };
   hp_result res;
-  hp_status st = hp_search(ctx, &f.prob, &opts, &res);
-  if (st != HP_OK) raise(ctx, st);
+  run(want_log ? HP_FLAG_LOG : 0, res);
 
   SearchOutcome out;
   out.candidates_simulated = res.candidates_simulated;
   out.candidates_pruned = res.candidates_pruned;
   if (want_log || !res.has_best) {
-    if (!want_log) {  // infeasible: the reasons come from the log
-      opts.flags = HP_FLAG_LOG;
-      st = hp_search(ctx, &f.prob, &opts, &res);
-      if (st != HP_OK) raise(ctx, st);
-    }
+    if (!want_log) run(HP_FLAG_LOG, res);  // infeasible: the reasons come from the log
     uint64_t n = 0, tb = 0;
-    if ((st = hp_search_log(ctx, nullptr, 0, nullptr, 0, &n, &tb)) != HP_OK) raise(ctx, st);
+    hp_status st;
+    auto get_log = [&](hp_log_entry* e, uint64_t ec, char* t, uint64_t tc) {
+      st = mg ? hp_multi_search_log(mg, e, ec, t, tc, &n, &tb) : hp_search_log(ctx, e, ec, t, tc, &n, &tb);
+      if (st != HP_OK) raise_msg(st, mg ? hp_multi_last_error(mg) : hp_last_error(ctx));
+    };
+    get_log(nullptr, 0, nullptr, 0);
     std::vector<hp_log_entry> ents(n);
     std::vector<char> text(tb);
-    if ((st = hp_search_log(ctx, ents.data(), n, text.data(), tb, &n, &tb)) != HP_OK) raise(ctx, st);
+    get_log(ents.data(), n, text.data(), tb);
     out.log.reserve(n);
     for (const hp_log_entry& e : ents)
       out.log.push_back({std::string(text.data() + e.candidate), e.time_s, std::string(text.data() + e.reason)});
@@ -205,8 +297,8 @@ SearchOutcome search(const ModelSpec& model, const ClusterSpec& cluster, const T
   }
   if (!want_log) out.log.clear();
   out.plan = unflatten(res.best_plan, cluster);
-  // The inner loop simulates without traces; give the winner a full one.
-  out.eval = evaluate_plan_unchecked(out.plan, model, cluster, cfg);
+  // the winner's full evaluation with trace, on the GPU
+  out.eval = evaluate_winner(ctx, f.prob, res.best_plan);
   return out;
 }
 

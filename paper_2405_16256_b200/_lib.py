@@ -53,6 +53,18 @@ def lib():
     l.hp_evaluate_plan_full.argtypes = [C.c_void_p, P(abi.hp_problem), P(abi.hp_plan), P(abi.hp_plan_eval),
                                         P(abi.hp_stage_eval), P(abi.hp_trace_event), C.c_uint64]
     l.hp_evaluate_plan_full.restype = C.c_int
+    l.hp_device_count.restype = C.c_int
+    l.hp_multi_create.argtypes = [P(C.c_void_p), P(C.c_int32), C.c_int32]
+    l.hp_multi_create.restype = C.c_int
+    l.hp_multi_destroy.argtypes = [C.c_void_p]
+    l.hp_multi_destroy.restype = None
+    l.hp_multi_last_error.argtypes = [C.c_void_p]
+    l.hp_multi_last_error.restype = C.c_char_p
+    l.hp_search_multi.argtypes = [C.c_void_p, P(abi.hp_problem), C.c_int32, P(abi.hp_result), P(abi.hp_result)]
+    l.hp_search_multi.restype = C.c_int
+    l.hp_multi_search_log.argtypes = [C.c_void_p, P(abi.hp_log_entry), C.c_uint64, C.c_char_p, C.c_uint64,
+                                      P(C.c_uint64), P(C.c_uint64)]
+    l.hp_multi_search_log.restype = C.c_int
     if l.hp_abi_version() != abi_version():
         raise NativeLibraryMissing("libhetplan_b200.so ABI version mismatch; rebuild")
     _lib = l
@@ -64,4 +76,5 @@ def abi_version() -> int:
 
 
 EXPORTED = ["hp_abi_version", "hp_create", "hp_destroy", "hp_last_error", "hp_validate", "hp_probe",
-            "hp_search", "hp_search_log", "hp_better_than", "hp_evaluate_plans", "hp_evaluate_plan_full"]
+            "hp_search", "hp_search_log", "hp_better_than", "hp_evaluate_plans", "hp_evaluate_plan_full",
+            "hp_device_count", "hp_multi_create", "hp_multi_destroy", "hp_multi_last_error", "hp_search_multi", "hp_multi_search_log"]

@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "--fmad=false", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
           "-I" + os.path.join(HERE, "..", "include")]
-SOURCES = ["hp_kernels.cu", "hp_host.cpp", "hp_log.cpp", "hp_eval.cpp", "hp_capi.cpp"]
+SOURCES = ["hp_kernels.cu", "hp_host.cpp", "hp_log.cpp", "hp_eval.cpp", "hp_capi.cpp", "hp_multi.cpp"]
 
 
 def _newest_dep_mtime() -> float:
@@ -56,7 +56,7 @@ def build(verbose: bool = False, ptxas_v: bool = False, out: str = OUT, defines=
 
     with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         objs = list(ex.map(compile_one, srcs))
-    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs]
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-ldl", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

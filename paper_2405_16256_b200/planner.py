@@ -142,6 +142,62 @@ class PlanEvaluation:
     trace: List[abi.hp_trace_event]
 
 
+class MultiEngine:
+    """hp_multi: one context per listed GPU in this process, NCCL between
+    them (include/hetplan_b200.h hp_search_multi)."""
+
+    def __init__(self, devices: List[int]):
+        self._lib = lib()
+        self._m = C.c_void_p()
+        arr = (C.c_int32 * len(devices))(*devices)
+        st = self._lib.hp_multi_create(C.byref(self._m), arr, len(devices))
+        if st != abi.HP_OK:
+            msg = (self._lib.hp_multi_last_error(self._m) or b"").decode()
+            self.close()
+            raise RuntimeError(f"hp_multi_create({devices}) failed with status {st}: {msg}")
+        self.devices = list(devices)
+
+    def close(self):
+        if self._m:
+            self._lib.hp_multi_destroy(self._m)
+            self._m = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search(self, problem: abi.Problem, flags: int = 0) -> Tuple[abi.hp_result, List[abi.hp_result]]:
+        red = abi.hp_result()
+        per = (abi.hp_result * len(self.devices))()
+        st = self._lib.hp_search_multi(self._m, problem.ptr(), flags, C.byref(red), per)
+        if st != abi.HP_OK:
+            msg = (self._lib.hp_multi_last_error(self._m) or b"").decode()
+            if st == abi.HP_BAD_CONFIG:
+                raise abi.ConfigError(msg)
+            raise RuntimeError(f"hp_search_multi failed (status {st}): {msg}")
+        return red, list(per)
+
+    def search_log(self) -> List[abi.SearchLogEntry]:
+        n, nb = C.c_uint64(), C.c_uint64()
+        st = self._lib.hp_multi_search_log(self._m, None, 0, None, 0, C.byref(n), C.byref(nb))
+        if st != abi.HP_OK:
+            raise RuntimeError((self._lib.hp_multi_last_error(self._m) or b"").decode())
+        ents = (abi.hp_log_entry * max(1, n.value))()
+        text = C.create_string_buffer(max(1, nb.value))
+        st = self._lib.hp_multi_search_log(self._m, ents, n.value, text, nb.value, C.byref(n), C.byref(nb))
+        if st != abi.HP_OK:
+            raise RuntimeError((self._lib.hp_multi_last_error(self._m) or b"").decode())
+        raw = text.raw
+        out = []
+        for k in range(n.value):
+            e = ents[k]
+            out.append(abi.SearchLogEntry(raw[e.candidate:raw.index(b"\0", e.candidate)].decode(), e.time_s,
+                                          raw[e.reason:raw.index(b"\0", e.reason)].decode()))
+        return out
+
+
 _engines: Dict[int, Engine] = {}
 
 

@@ -81,6 +81,23 @@ def test_dropin_library_matches_reference(dropin, search_cases):
         assert _digest(r["log"]) == logs[case["name"]]["sha256"], case["name"]
 
 
+def test_dropin_winner_evaluation_matches_reference(dropin, search_cases):
+    """SearchOutcome.eval (planner.cpp:681-684) comes from the B200 engine
+    (hp_evaluate_plan_full), equal to the reference's PlanEvaluation: stage
+    costs, compute ends, peak in-flight / memory, pipeline time, bubbles."""
+    from oracle import ref
+    n = 0
+    for case in search_cases:
+        if case["status"] != 0:
+            continue
+        got = dropin(case["docs"])["eval"]
+        want = ref.search(case["docs"])["eval"]
+        assert got == want, case["name"]
+        n += 1
+        if n >= 60:
+            break
+
+
 def _write_inputs(d, docs):
     paths = {}
     for k in ("model", "cluster", "train", "planner"):
