@@ -13,9 +13,11 @@
 // loadable without it; only hp_multi_create needs it.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -117,7 +119,18 @@ hp_status hp_multi_create(hp_multi** out, const int32_t* devices, int32_t n) {
     }
   }
   m->comm.assign(n, nullptr);
+  // NCCL prints its version banner on stdout at initialisation when
+  // NCCL_DEBUG is set; a library must not write on the host program's stdout
+  // (the CLI's report goes there), so fd 1 points at stderr for the call
+  std::fflush(stdout);
+  const int saved = dup(1);
+  if (saved >= 0) dup2(2, 1);
   ncclResult_t nr = g_nccl.init_all(m->comm.data(), n, m->devices.data());
+  std::fflush(stdout);
+  if (saved >= 0) {
+    dup2(saved, 1);
+    close(saved);
+  }
   *out = m;
   if (nr != ncclSuccess) return set_err(m, HP_NCCL, std::string("ncclCommInitAll: ") + g_nccl.error_string(nr));
   return HP_OK;

@@ -113,7 +113,10 @@ def _run_plan(binary, paths, out):
            "--planner", paths["planner"], "--out", out, "--jobs", "4"]
     if "profiles" in paths:
         cmd += ["--profiles", paths["profiles"]]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    # NCCL_DEBUG asks NCCL (the drop-in's multi-GPU path, --jobs > 1) to print
+    # its own diagnostics on stderr; compare the planners' output without it
+    env = {k: v for k, v in os.environ.items() if k != "NCCL_DEBUG"}
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     files = {}
     for name in ("plan.json", "report.json", "search_log.ndjson"):
         fp = os.path.join(out, name)
