@@ -27,10 +27,9 @@
 extern "C" {
 #endif
 
-#define HP_ABI_VERSION 2
-#define HP_MAX_GROUPS 8      /* device groups (accelerator types) per cluster */
+#define HP_ABI_VERSION 3
+#define HP_MAX_GROUPS 16     /* device groups (accelerator types) per cluster */
 #define HP_MAX_STAGES 256    /* pipeline stages per plan */
-#define HP_NAME_LEN 32
 
 typedef enum hp_status {
   HP_OK = 0,
@@ -60,7 +59,7 @@ typedef struct hp_model {
 
 /* DeviceGroup, types.hpp:47-61 */
 typedef struct hp_group {
-  char name[HP_NAME_LEN];
+  const char* name; /* NUL-terminated UTF-8, any length; borrowed for the call */
   double peak_tflops;
   double memory_bytes;
   int32_t node_count;
@@ -71,7 +70,11 @@ typedef struct hp_group {
 
 /* Link + LinkScope, types.hpp:67-88; groups referenced by index into
  * hp_cluster.groups (the reference stores names and resolves them by linear
- * scan, types.cpp:26-56). group_b is ignored unless scope == HP_INTER_GROUP. */
+ * scan, types.cpp:26-56). group_b is ignored unless scope == HP_INTER_GROUP.
+ * A caller resolving names passes -1 for a name no group has and, optionally,
+ * the name itself in group_a_name / group_b_name, so validation reports it
+ * like the reference ("link references unknown group '<name>'",
+ * types.cpp:126-135); both may be NULL. */
 typedef struct hp_link {
   int32_t scope;
   int32_t path;
@@ -81,6 +84,8 @@ typedef struct hp_link {
   double latency_s;
   double efficiency;
   double staging_copy_bytes_per_s;
+  const char* group_a_name;
+  const char* group_b_name;
 } hp_link;
 
 /* ClusterSpec, types.hpp:90-103 */

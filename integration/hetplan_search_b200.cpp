@@ -69,10 +69,7 @@ void flatten(const ModelSpec& m, const ClusterSpec& c, const TrainConfig& t, con
   hm.edge_layer_cost_multiplier = m.edge_layer_cost_multiplier;
   for (const DeviceGroup& g : c.groups) {
     hp_group h{};
-    if (g.name.size() >= HP_NAME_LEN)
-      throw ConfigError("cluster: group name '" + g.name + "' longer than " +
-                        std::to_string(HP_NAME_LEN - 1) + " bytes");
-    std::memcpy(h.name, g.name.data(), g.name.size());
+    h.name = g.name.c_str();  // borrowed: the specs outlive the call
     h.peak_tflops = g.peak_tflops;
     h.memory_bytes = g.memory_bytes;
     h.node_count = g.node_count;
@@ -89,6 +86,8 @@ void flatten(const ModelSpec& m, const ClusterSpec& c, const TrainConfig& t, con
     h.path = l.path_kind == PathKind::CpuStaged ? HP_CPU_STAGED : HP_GPU_DIRECT;
     h.group_a = group_index(c, l.endpoints.group_a);
     h.group_b = l.endpoints.kind == ScopeKind::InterGroup ? group_index(c, l.endpoints.group_b) : -1;
+    h.group_a_name = l.endpoints.group_a.c_str();
+    h.group_b_name = l.endpoints.group_b.c_str();
     h.bandwidth_bits_per_s = l.bandwidth_bits_per_s;
     h.latency_s = l.latency_s;
     h.efficiency = l.efficiency;

@@ -473,7 +473,10 @@ typedef struct task_result {
 
 /* encode_plan, planner.cpp:192-200 */
 static char* encode_plan(const hp_problem* pr, const hp_plan* p) {
-  size_t cap = 64 + (size_t)p->n_stages * (HP_NAME_LEN + 64);
+  size_t longest = 0;
+  for (int g = 0; g < pr->cluster.n_groups; ++g)
+    if (strlen(pr->cluster.groups[g].name) > longest) longest = strlen(pr->cluster.groups[g].name);
+  size_t cap = 64 + (size_t)p->n_stages * (longest + 64);
   char* s = malloc(cap);
   size_t n = (size_t)snprintf(s, cap, "%s|%lld|%lld", p->schedule == HP_GPIPE ? "gpipe" : "1f1b",
                               (long long)p->micro_batches_per_dp_replica,

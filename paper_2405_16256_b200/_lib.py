@@ -72,7 +72,7 @@ def lib():
 
 
 def abi_version() -> int:
-    return 2
+    return 3
 
 
 EXPORTED = ["hp_abi_version", "hp_create", "hp_destroy", "hp_last_error", "hp_validate", "hp_probe",

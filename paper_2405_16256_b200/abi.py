@@ -13,9 +13,8 @@ import ctypes as C
 import math
 from typing import Dict, List, NamedTuple, Tuple
 
-HP_MAX_GROUPS = 8
+HP_MAX_GROUPS = 16
 HP_MAX_STAGES = 256
-HP_NAME_LEN = 32
 
 HP_OK, HP_BAD_CONFIG, HP_INFEASIBLE, HP_CUDA, HP_NCCL, HP_INTERNAL = range(6)
 HP_GPIPE, HP_1F1B = 0, 1
@@ -35,7 +34,7 @@ class hp_model(C.Structure):
 
 
 class hp_group(C.Structure):
-    _fields_ = [("name", C.c_char * HP_NAME_LEN), ("peak_tflops", C.c_double), ("memory_bytes", C.c_double),
+    _fields_ = [("name", C.c_char_p), ("peak_tflops", C.c_double), ("memory_bytes", C.c_double),
                 ("node_count", C.c_int32), ("devices_per_node", C.c_int32),
                 ("compute_efficiency", C.c_double), ("bwd_fwd_ratio", C.c_double)]
 
@@ -43,7 +42,7 @@ class hp_group(C.Structure):
 class hp_link(C.Structure):
     _fields_ = [("scope", C.c_int32), ("path", C.c_int32), ("group_a", C.c_int32), ("group_b", C.c_int32),
                 ("bandwidth_bits_per_s", C.c_double), ("latency_s", C.c_double), ("efficiency", C.c_double),
-                ("staging_copy_bytes_per_s", C.c_double)]
+                ("staging_copy_bytes_per_s", C.c_double), ("group_a_name", C.c_char_p), ("group_b_name", C.c_char_p)]
 
 
 class hp_cluster(C.Structure):
@@ -179,14 +178,14 @@ class Problem:
         if len(groups) > HP_MAX_GROUPS:
             raise ConfigError(f"cluster: at most {HP_MAX_GROUPS} device groups supported")
         self.group_names: List[str] = []
+        self._keep: List[bytes] = []  # name buffers the structs point into
         self._groups = (hp_group * max(1, len(groups)))()
         for i, g in enumerate(groups):
             name = str(_req(g, "name", "cluster.group"))
-            if len(name.encode()) >= HP_NAME_LEN:
-                raise ConfigError(f"cluster: group name '{name}' longer than {HP_NAME_LEN - 1} bytes")
             self.group_names.append(name)
             G = self._groups[i]
-            G.name = name.encode()
+            self._keep.append(name.encode())
+            G.name = self._keep[-1]
             G.peak_tflops = float(_req(g, "peak_tflops", "cluster.group"))
             G.memory_bytes = float(_req(g, "memory_bytes", "cluster.group"))
             G.node_count = int(_req(g, "node_count", "cluster.group"))
@@ -211,9 +210,13 @@ class Problem:
             if L.scope == HP_INTER_GROUP:
                 a, b = _req(ep, "group_a", "cluster.link"), _req(ep, "group_b", "cluster.link")
                 L.group_a, L.group_b = idx.get(a, -1), idx.get(b, -1)
+                self._keep += [str(a).encode(), str(b).encode()]
+                L.group_a_name, L.group_b_name = self._keep[-2], self._keep[-1]
             else:
                 a = _req(ep, "group", "cluster.link")
                 L.group_a, L.group_b = idx.get(a, -1), -1
+                self._keep.append(str(a).encode())
+                L.group_a_name = self._keep[-1]
             L.bandwidth_bits_per_s = float(_req(l, "bandwidth_bits_per_s", "cluster.link"))
             L.latency_s = float(l.get("latency_s", 0.0))
             pk = l.get("path_kind", "gpu-direct")

@@ -28,8 +28,7 @@
 
 namespace hpc {
 
-constexpr int MAXG = 8;      // device groups
-constexpr int NAMELEN = 32;
+constexpr int MAXG = 16;     // device groups (HP_MAX_GROUPS)
 
 // Problem-wide constants (one per search), __constant__ on the device.
 struct Consts {
@@ -48,7 +47,10 @@ struct Consts {
   int link_pair[MAXG][MAXG];  // inter-group link of (g, h), -1 if none
   int n_links;
   int n_B;               // micro-batch candidates
-  char names[MAXG][NAMELEN];
+  // group names for encode_plan (tie-break): names + name_off[g], name_len[g]
+  // bytes; `names` points at a device copy on the GPU (the caller sets it)
+  const char* names;
+  int name_off[MAXG];
   int name_len[MAXG];
 };
 
@@ -381,7 +383,7 @@ HPD int enc_next(EncStream& e) {
     switch (e.field) {
       case 5: e.field = 6; e.pos = 0; return '|';
       case 6:
-        if (e.pos < e.c->name_len[g]) return (unsigned char)e.c->names[g][e.pos++];
+        if (e.pos < e.c->name_len[g]) return (unsigned char)e.c->names[e.c->name_off[g] + e.pos++];
         e.field = 7; e.pos = 0; continue;
       case 7: case 11: case 13: case 15:
         e.field++; e.pos = 0; e.numlen = -1;

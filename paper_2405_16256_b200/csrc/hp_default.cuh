@@ -28,7 +28,9 @@ struct TaskRes {
   int has_best, best_leaf;
 };
 
-// Per-warp scratch (global memory), CH entries each.
+// Per-block scratch (global memory): CH entries each for the candidates of
+// one batch; 2*SC entries (SC = most leaves in a task) for the seeds of
+// every leaf of the task.
 struct DefScratch {
   long long* ids;
   double* lower;
@@ -36,9 +38,17 @@ struct DefScratch {
   unsigned char* flag;  // bit0 valid, bit1 mem_ok, bit2 old
   double* dec;          // per-slot decision of a hill step (time or -1)
   int CH;
+  unsigned char* sflag; // seeds: flag bits, bit3 = proportional equals uniform (memo hit)
+  double* slow;         // seeds: lower bounds
+  int SC;
 };
 
 constexpr int DEF_CH = 1024;
+#ifndef HP_DEF_WARPS
+#define HP_DEF_WARPS 4  // warps per task (tuning)
+#endif
+constexpr int DEF_WARPS = HP_DEF_WARPS;
+constexpr int DEF_THREADS = 32 * DEF_WARPS;
 
 // Lower bound and memory gate of one candidate (serial over stages).
 // Returns flag bits (valid | mem_ok) and the bound.
@@ -99,9 +109,17 @@ __device__ inline void take_best(const Bufs& b, TaskState& ts, int* tbest, int l
                                  double t) {
   bool better = !ts.has_best || t < ts.best_t;
   if (!better && t == ts.best_t) {
-    const Leaf la = b.leaves[li], lb = b.leaves[ts.best_leaf];
-    better = cand_less(c_consts, t, la, b.lg + la.lg_off, b.layouts + la.layout_off, split, ts.best_t,
-                       lb, b.lg + lb.lg_off, b.layouts + lb.layout_off, tbest);
+    const Leaf la = b.leaves[li];
+    if (li == ts.best_leaf) {
+      // same leaf: the encodings differ first at the first differing stage
+      // end (split_enc_less, hp_search_core.cuh) — exact ties are common
+      // between identical stages, so this is the hot case
+      better = split_enc_less(la.P, split, tbest);
+    } else {
+      const Leaf lb = b.leaves[ts.best_leaf];
+      better = cand_less(c_consts, t, la, b.lg + la.lg_off, b.layouts + la.layout_off, split, ts.best_t,
+                         lb, b.lg + lb.lg_off, b.layouts + lb.layout_off, tbest);
+    }
   }
   if (better) {
     ts.has_best = 1;
@@ -116,14 +134,15 @@ __device__ inline double incumbent(const TaskState& ts, double gb) {
   return ts.has_best && ts.best_t < gb ? ts.best_t : gb;
 }
 
-// Simulates the candidates ids[0..n) of kind `kind` for leaf li (any order),
-// cpw per warp pass. Results land where eval_item writes them.
+// Simulates the candidates ids[0..n) of kind `kind` for leaf li (any order)
+// on the block's warps, cpw per warp pass. Results land where eval_item
+// writes them; the caller syncs the block before and after.
 __device__ inline void simulate_list(const Bufs& b, int li, int kind, const long long* ids, int n,
-                                     int out_base, int lane) {
+                                     int out_base, int warp, int lane) {
   const Leaf lf = b.leaves[li];
   const int cls = eval_class(lf.P, lf.M, lf.sched == 0);
   const int cpw = class_cpw(cls, lf.P);
-  for (int g = 0; g < n; g += cpw) {
+  for (int g = warp * cpw; g < n; g += DEF_WARPS * cpw) {
     Work w;
     w.leaf = li;
     w.kind = kind;
@@ -133,38 +152,94 @@ __device__ inline void simulate_list(const Bufs& b, int li, int kind, const long
     w.ids = ids;
     eval_dispatch(cls, b, w, lane);
   }
-  __syncwarp();
 }
 
-__global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, int n_tasks,
-                                                 int* next_task, TaskRes* res, int* tbest_rows,
-                                                 DefScratch sc, double global_bound, int probe,
-                                                 int uniform_only) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  long long* ids = sc.ids + (size_t)gw * sc.CH;
-  double* lower = sc.lower + (size_t)gw * sc.CH;
-  unsigned char* flag = sc.flag + (size_t)gw * sc.CH;
-  double* dec = sc.dec + (size_t)gw * sc.CH;
+// One block of DEF_WARPS warps per task, tasks pulled in `order` (longest
+// expected first). The task's leaves run in reference order; per leaf every
+// batch (the seeds, a hill-climb neighbourhood, a chunk of exhaustive
+// compositions) is gated by all threads and the candidates the batch-start
+// incumbent does not exclude are simulated by all warps (speculatively: the
+// incumbent only decreases, so this is a superset of what the reference
+// simulates), then thread 0 replays the batch in the reference's order with
+// the evolving incumbent (planner.cpp:425-551). The seeds of every leaf and
+// their gates are incumbent-free and computed for the whole task at once.
+// probe: the probe pass (planner.cpp:640-651): stop a task at its first
+// simulated seed and fold its time into *gb_bits (atomic min of the bit
+// patterns of non-negative doubles); otherwise *gb_bits is the global bound.
+__global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs b, const TaskDev* tasks, const int* order, int n_tasks,
+                                                        int* next_task, TaskRes* res, int* tbest_rows, DefScratch sc,
+                                                        unsigned long long* gb_bits, int probe, int uniform_only) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  long long* ids = sc.ids + (size_t)blockIdx.x * sc.CH;  // global: the evaluators read it
+  // batch decisions in shared memory: thread 0's in-order replay reads them
+  // back serially, so they must be a few cycles away, not an L2 round trip
+  __shared__ double lower[DEF_CH];
+  __shared__ double dec[DEF_CH];
+  __shared__ unsigned char flag[DEF_CH];
+  unsigned char* sflag = sc.sflag + (size_t)blockIdx.x * 2 * sc.SC;
+  double* slow = sc.slow + (size_t)blockIdx.x * 2 * sc.SC;
   Bufs bx = b;
   bx.xbuf = sc.times;
-  const int xbase = gw * sc.CH;
+  const int xbase = blockIdx.x * sc.CH;
   const bool pruning = c_consts.pruning != 0;
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  __shared__ int s_task, s_cnt, s_stop, s_moved;
+  __shared__ double s_inc, s_dseed[2], s_cur_t;
 
   for (;;) {
-    int task = 0;
-    if (lane == 0) task = atomicAdd(next_task, 1);
-    task = __shfl_sync(0xffffffffu, task, 0);
-    if (task >= n_tasks) return;
+    if (tid == 0) s_task = atomicAdd(next_task, 1);
+    __syncthreads();
+    const int kpos = s_task;
+    if (kpos >= n_tasks) return;
+    const int task = order[kpos];
     const TaskDev td = tasks[task];
     int* tbest = tbest_rows + td.best_off;
-    TaskState ts{0.0, 0, -1, 0, 0, 0};
-    const double gb = probe ? INF : global_bound;
-    int lseq = 0;  // search-log segment counter of this task (lane 0)
+    TaskState ts{0.0, 0, -1, 0, 0, 0};  // meaningful in thread 0
+    const double gb = probe ? INF : __longlong_as_double(*(volatile long long*)gb_bits);
+    int lseq = 0;  // search-log segment counter of this task (thread 0)
     const bool logging = b.log.vals != nullptr && !probe;
+    // HP_DEBUG_TASKS: per task (cycles, leaves, hill steps, simulations)
+    const long long dbg_t0 = b.trace ? clock64() : 0;
+    long long dbg_steps = 0;
+    long long dbg_sim = 0, dbg_gate = 0, dbg_rep = 0, dbg_seed = 0, dbg_c = 0, dbg_mo = 0;
+#define DBG_MARK(acc)                  \
+  if (b.trace) {                       \
+    const long long now_ = clock64();  \
+    acc += now_ - dbg_c;               \
+    dbg_c = now_;                      \
+  }
+    if (b.trace) dbg_c = clock64();
 
-    for (int li = td.leaf_begin; li < td.leaf_end; ++li) {
+    // ---- seeds of every leaf and their gates (incumbent-free)
+    const int nl = td.leaf_end - td.leaf_begin;
+    for (int j = tid; j < nl; j += DEF_THREADS) {
+      const int li = td.leaf_begin + j;
+      const Leaf lf = b.leaves[li];
+      const LeafGroup* lg = b.lg + lf.lg_off;
+      const uint8_t* slots = b.layouts + lf.layout_off;
+      const double* hop = b.hop + lf.B_idx * c_consts.n_links;
+      int* uni = b.uni + lf.split_off;
+      int* prop = b.prop + lf.split_off;
+      double w[HP_MAX_STAGES], frac[HP_MAX_STAGES];
+      int ord[HP_MAX_STAGES];
+      seed_splits(c_consts, lf, lg, slots, uni, prop, w, frac, ord);
+      double lo = 0.0;
+      sflag[2 * j] = cand_gate(c_consts, lf, lg, slots, hop, uni, &lo);
+      slow[2 * j] = lo;
+      if (same_split(uni, prop, lf.P)) {
+        sflag[2 * j + 1] = 8;
+        slow[2 * j + 1] = 0.0;
+      } else {
+        sflag[2 * j + 1] = cand_gate(c_consts, lf, lg, slots, hop, prop, &lo);
+        slow[2 * j + 1] = lo;
+      }
+    }
+    __syncthreads();
+    DBG_MARK(dbg_seed)
+
+    for (int j = 0; j < nl; ++j) {
+      const int li = td.leaf_begin + j;
       const Leaf lf = b.leaves[li];
       const int P = lf.P;
       const LeafGroup* lg = b.lg + lf.lg_off;
@@ -172,58 +247,57 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
       const double* hop = b.hop + lf.B_idx * c_consts.n_links;
       int* uni = b.uni + lf.split_off;
       int* prop = b.prop + lf.split_off;
-      if (lane == 0) {
-        double w[HP_MAX_STAGES], frac[HP_MAX_STAGES];
-        int order[HP_MAX_STAGES];
-        seed_splits(c_consts, lf, lg, slots, uni, prop, w, frac, order);
-      }
-      __syncwarp();
-
-      // ---- seeds, decided one at a time (planner.cpp:435-451)
-      double dseed[2] = {-1.0, -1.0};
-      const bool prop_same = same_split(uni, prop, P);
       const int nseed = uniform_only ? 1 : 2;
-      for (int s = 0; s < nseed; ++s) {
-        if (s == 1 && prop_same) {  // memo hit
-          dseed[1] = dseed[0];
-          continue;
+
+      // ---- seeds (planner.cpp:435-451): simulate those the incumbent at the
+      // leaf's start admits, then decide them one at a time
+      if (tid == 0) {
+        const double inc0 = incumbent(ts, gb);
+        int n = 0;
+        for (int s = 0; s < nseed; ++s) {
+          const unsigned char f = sflag[2 * j + s];
+          if (f & 8) continue;
+          if ((f & 2) && !(pruning && inc0 < INF && slow[2 * j + s] > inc0)) ids[n++] = s;
         }
-        const int* split = s == 0 ? uni : prop;
-        double lo = 0.0;
-        unsigned char fl = 0;
-        if (lane == 0) fl = cand_gate(c_consts, lf, lg, slots, hop, split, &lo);
-        fl = __shfl_sync(0xffffffffu, fl, 0);
-        lo = __shfl_sync(0xffffffffu, lo, 0);
-        double inc = incumbent(ts, gb);
-        int act;  // 0 mem, 1 bound, 2 simulate
-        if (!(fl & 2)) act = 0;
-        else if (pruning && inc < INF && lo > inc) act = 1;
-        else act = 2;
-        if (act == 2) {
-          long long id = s;
-          if (lane == 0) ids[0] = id;
-          __syncwarp();
-          simulate_list(bx, li, 0, ids, 1, xbase, lane);
-          double t = b.tseed[2 * li + s];
-          dseed[s] = t;
-          if (lane == 0) {
+        s_cnt = n;
+      }
+      __syncthreads();
+      DBG_MARK(dbg_rep)
+      if (s_cnt > 0) simulate_list(bx, li, 0, ids, s_cnt, xbase, warp, lane);
+      __syncthreads();
+      DBG_MARK(dbg_sim)
+      if (tid == 0) {
+        double dseed[2] = {-1.0, -1.0};
+        for (int s = 0; s < nseed; ++s) {
+          const unsigned char f = sflag[2 * j + s];
+          if (f & 8) {  // memo hit (planner.cpp:425-432)
+            dseed[1] = dseed[0];
+            continue;
+          }
+          const double inc = incumbent(ts, gb);
+          if (!(f & 2)) {
+            ts.pmem++;
+          } else if (pruning && inc < INF && slow[2 * j + s] > inc) {
+            ts.pbound++;
+          } else {
+            const double t = b.tseed[2 * li + s];
+            dseed[s] = t;
             ts.sim++;
-            take_best(b, ts, tbest, li, split, t);
+            take_best(b, ts, tbest, li, s == 0 ? uni : prop, t);
             if (logging) {
               const long long off = log_reserve(b.log, task, lseq++, 1);
               if (off >= 0) b.log.vals[off] = t;
             }
           }
-        } else if (lane == 0) {
-          if (act == 0) ts.pmem++;
-          else ts.pbound++;
         }
-        ts.best_t = __shfl_sync(0xffffffffu, ts.best_t, 0);
-        ts.has_best = __shfl_sync(0xffffffffu, ts.has_best, 0);
-        ts.best_leaf = __shfl_sync(0xffffffffu, ts.best_leaf, 0);
+        s_dseed[0] = dseed[0];
+        s_dseed[1] = dseed[1];
+        s_stop = probe && ts.sim > 0;
       }
+      __syncthreads();
+      DBG_MARK(dbg_seed)
       if (probe) {
-        if (__shfl_sync(0xffffffffu, (int)(ts.sim > 0), 0)) break;
+        if (s_stop) break;
         continue;
       }
       if (uniform_only) continue;
@@ -232,18 +306,19 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
         // ---- exhaustive, in rank order (planner.cpp:454-459)
         const long long total = contiguous_split_count(c_consts.L, P);
         long long ru = 0, rp = 0;
-        if (lane == 0) {
-          ru = rank_composition(uni, c_consts.L, P);
-          rp = rank_composition(prop, c_consts.L, P);
-        }
-        ru = __shfl_sync(0xffffffffu, ru, 0);
-        rp = __shfl_sync(0xffffffffu, rp, 0);
+        ru = rank_composition(uni, c_consts.L, P);
+        rp = rank_composition(prop, c_consts.L, P);
         for (long long base = 0; base < total; base += sc.CH) {
           const int n = (int)min((long long)sc.CH, total - base);
-          const double inc0 = incumbent(ts, gb);
-          // gate all candidates of the chunk: lane-contiguous rank ranges
-          const int per = (n + 31) / 32;
-          const int lo_k = lane * per, hi_k = min(n, lo_k + per);
+          if (tid == 0) {
+            s_inc = incumbent(ts, gb);
+            s_cnt = 0;
+          }
+          __syncthreads();
+          const double inc0 = s_inc;
+          // gate: thread-contiguous rank ranges; survivors get a result slot
+          const int per = (n + DEF_THREADS - 1) / DEF_THREADS;
+          const int lo_k = tid * per, hi_k = min(n, lo_k + per);
           if (lo_k < hi_k) {
             int comp[HP_MAX_STAGES];
             unrank_composition(base + lo_k, c_consts.L, P, comp);
@@ -251,68 +326,51 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
               if (k > lo_k) next_composition(comp, P);
               double l;
               unsigned char f = cand_gate(c_consts, lf, lg, slots, hop, comp, &l);
-              long long r = base + k;
+              const long long r = base + k;
               if (r == ru || r == rp) f |= 4;  // memo: seeds already decided
               flag[k] = f;
               lower[k] = l;
+              if ((f & 1) && (f & 2) && !(f & 4) && !(pruning && inc0 < INF && l > inc0)) {
+                const int pos = atomicAdd(&s_cnt, 1);
+                ids[pos] = r;
+                dec[k] = (double)pos;  // where its time will land
+              }
             }
           }
-          __syncwarp();
-          // survivors (ordered compaction not needed: results are indexed)
-          int cnt = 0;
-          for (int k0 = 0; k0 < n; k0 += 32) {
-            const int k = k0 + lane;
-            bool surv = false;
-            if (k < n) {
-              unsigned char f = flag[k];
-              surv = (f & 1) && (f & 2) && !(f & 4) && !(pruning && inc0 < INF && lower[k] > inc0);
-            }
-            unsigned m = __ballot_sync(0xffffffffu, surv);
-            if (surv) {
-              int pos = cnt + __popc(m & ((1u << lane) - 1u));
-              ids[pos] = base + k;
-              dec[k] = (double)pos;  // where its time will land
-            }
-            cnt += __popc(m);
-          }
-          __syncwarp();
-          if (cnt > 0) simulate_list(bx, li, 2, ids, cnt, xbase, lane);
-          if (lane == 0) {
+          __syncthreads();
+          const int cnt = s_cnt;
+          if (cnt > 0) simulate_list(bx, li, 2, ids, cnt, xbase, warp, lane);
+          __syncthreads();
+          if (tid == 0) {
             int comp[HP_MAX_STAGES];
-            bool have_comp = false;
             int nv = 0;  // simulated times, compacted into dec[0..nv) (nv <= k: not yet read)
             for (int k = 0; k < n; ++k) {
-              unsigned char f = flag[k];
+              const unsigned char f = flag[k];
               if (f & 4) continue;  // memo hit
               if (!(f & 2)) {
                 ts.pmem++;
                 continue;
               }
-              double inc = incumbent(ts, gb);
+              const double inc = incumbent(ts, gb);
               if (pruning && inc < INF && lower[k] > inc) {
                 ts.pbound++;
                 continue;
               }
-              double t = sc.times[xbase + (int)dec[k]];
+              const double t = sc.times[xbase + (int)dec[k]];
               dec[nv++] = t;
               ts.sim++;
               if (!ts.has_best || t <= ts.best_t) {
                 unrank_composition(base + k, c_consts.L, P, comp);
-                have_comp = true;
                 take_best(b, ts, tbest, li, comp, t);
               }
             }
-            (void)have_comp;
             if (logging) {
-              long long off = log_reserve(b.log, task, lseq++, nv);
+              const long long off = log_reserve(b.log, task, lseq++, nv);
               if (off >= 0)
-                for (int j = 0; j < nv; ++j) b.log.vals[off + j] = dec[j];
+                for (int q = 0; q < nv; ++q) b.log.vals[off + q] = dec[q];
             }
           }
-          ts.best_t = __shfl_sync(0xffffffffu, ts.best_t, 0);
-          ts.has_best = __shfl_sync(0xffffffffu, ts.has_best, 0);
-          ts.best_leaf = __shfl_sync(0xffffffffu, ts.best_leaf, 0);
-          __syncwarp();
+          __syncthreads();
         }
         continue;
       }
@@ -320,70 +378,65 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
       // ---- steepest descent (planner.cpp:461-489)
       int* cur = b.cur + lf.split_off;
       short* hist = b.hist + b.hist_off[li];
-      double cur_t;
+      const double ds0 = s_dseed[0], ds1 = s_dseed[1];
+      double cur_t = 0.0;
       int start = 0;
-      if (dseed[1] >= 0) {
+      if (ds1 >= 0) {
         start = 1;
-        cur_t = dseed[1];
-      } else if (dseed[0] >= 0) {
+        cur_t = ds1;
+      } else if (ds0 >= 0) {
         start = 2;
-        cur_t = dseed[0];
+        cur_t = ds0;
       }
       if (start == 0) continue;
-      if (lane == 0)
-        for (int i = 0; i < P; ++i) cur[i] = start == 1 ? prop[i] : uni[i];
-      __syncwarp();
+      for (int i = tid; i < P; i += DEF_THREADS) cur[i] = start == 1 ? prop[i] : uni[i];
       const int nslots = 2 * (P - 1);
       const int max_steps = 4 * c_consts.L;
       for (int step = 0; step < max_steps; ++step) {
-        const double inc0 = incumbent(ts, gb);
-        // old flags (memo) by lane 0
-        if (lane == 0) {
+        __syncthreads();
+        // old flags (memo) by thread 0
+        if (tid == 0) {
           int delta[HP_MAX_STAGES];
           for (int i = 0; i < P; ++i) delta[i] = 0;
           unsigned char old[2 * HP_MAX_STAGES];
           mark_old(lf, cur, uni, prop, hist, step, delta, old);
           for (int q = 0; q < nslots; ++q) flag[q] = old[q] ? 4 : 0;
+          s_inc = incumbent(ts, gb);
+          s_cnt = 0;
         }
-        __syncwarp();
-        // gate every neighbour
-        for (int q = lane; q < nslots; q += 32) {
+        __syncthreads();
+        DBG_MARK(dbg_mo)
+        const double inc0 = s_inc;
+        // gate every neighbour; list the ones to simulate
+        for (int q = tid; q < nslots; q += DEF_THREADS) {
           int nbs[HP_MAX_STAGES];
           const int bb = q >> 1, d = (q & 1) ? -1 : 1;
           for (int i = 0; i < P; ++i) nbs[i] = cur[i];
           nbs[bb] += d;
           nbs[bb + 1] -= d;
           double l = 0.0;
-          unsigned char f = (nbs[bb] >= 1 && nbs[bb + 1] >= 1)
-                                ? cand_gate(c_consts, lf, lg, slots, hop, nbs, &l) : 0;
-          flag[q] |= f;
+          const unsigned char f0 = (nbs[bb] >= 1 && nbs[bb + 1] >= 1)
+                                       ? cand_gate(c_consts, lf, lg, slots, hop, nbs, &l) : 0;
+          const unsigned char f = flag[q] | f0;
+          flag[q] = f;
           lower[q] = l;
+          if ((f & 1) && (f & 2) && !(f & 4) && !(pruning && inc0 < INF && l > inc0)) ids[atomicAdd(&s_cnt, 1)] = q;
         }
-        __syncwarp();
-        int cnt = 0;
-        for (int q0 = 0; q0 < nslots; q0 += 32) {
-          const int q = q0 + lane;
-          bool surv = false;
-          if (q < nslots) {
-            unsigned char f = flag[q];
-            surv = (f & 1) && (f & 2) && !(f & 4) && !(pruning && inc0 < INF && lower[q] > inc0);
-          }
-          unsigned m = __ballot_sync(0xffffffffu, surv);
-          if (surv) ids[cnt + __popc(m & ((1u << lane) - 1u))] = q;
-          cnt += __popc(m);
-        }
-        __syncwarp();
-        if (cnt > 0) simulate_list(bx, li, 1, ids, cnt, xbase, lane);
-        int moved = 0;
-        if (lane == 0) {
+        __syncthreads();
+        DBG_MARK(dbg_gate)
+        const int cnt = s_cnt;
+        if (cnt > 0) simulate_list(bx, li, 1, ids, cnt, xbase, warp, lane);
+        __syncthreads();
+        DBG_MARK(dbg_sim)
+        if (tid == 0) {
           const double* nbt = b.nb + b.nb_off[li];
           int nbs[HP_MAX_STAGES];
           int bq = -1;
           double bt = 0.0;
           int nv = 0;
-          // memo values of neighbours equal to the seeds
+          int moved = 0;
           for (int q = 0; q < nslots; ++q) {
-            unsigned char f = flag[q];
+            const unsigned char f = flag[q];
             if (!(f & 1)) continue;  // count < 1: skipped by the reference (:478)
             double t = -1.0;
             const int bb = q >> 1, d = (q & 1) ? -1 : 1;
@@ -392,12 +445,12 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
               for (int i = 0; i < P; ++i) nbs[i] = cur[i];
               nbs[bb] += d;
               nbs[bb + 1] -= d;
-              if (same_split(nbs, uni, P)) t = dseed[0];
-              else if (same_split(nbs, prop, P)) t = dseed[1];
+              if (same_split(nbs, uni, P)) t = ds0;
+              else if (same_split(nbs, prop, P)) t = ds1;
             } else if (!(f & 2)) {
               ts.pmem++;
             } else {
-              double inc = incumbent(ts, gb);
+              const double inc = incumbent(ts, gb);
               if (pruning && inc < INF && lower[q] > inc) {
                 ts.pbound++;
               } else {
@@ -418,9 +471,9 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
             }
           }
           if (logging) {
-            long long off = log_reserve(b.log, task, lseq++, nv);
+            const long long off = log_reserve(b.log, task, lseq++, nv);
             if (off >= 0)
-              for (int j = 0; j < nv; ++j) b.log.vals[off + j] = dec[j];
+              for (int q = 0; q < nv; ++q) b.log.vals[off + q] = dec[q];
           }
           if (bq >= 0 && bt < cur_t) {
             const int bb = bq >> 1, d = (bq & 1) ? -1 : 1;
@@ -430,17 +483,17 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
             cur_t = bt;
             moved = 1;
           }
+          s_moved = moved;
+          s_cur_t = cur_t;
         }
-        moved = __shfl_sync(0xffffffffu, moved, 0);
-        cur_t = __shfl_sync(0xffffffffu, cur_t, 0);
-        ts.best_t = __shfl_sync(0xffffffffu, ts.best_t, 0);
-        ts.has_best = __shfl_sync(0xffffffffu, ts.has_best, 0);
-        ts.best_leaf = __shfl_sync(0xffffffffu, ts.best_leaf, 0);
-        __syncwarp();
-        if (!moved) break;
+        __syncthreads();
+        DBG_MARK(dbg_rep)
+        ++dbg_steps;
+        cur_t = s_cur_t;
+        if (!s_moved) break;
       }
     }
-    if (lane == 0) {
+    if (tid == 0) {
       TaskRes r;
       r.best_time = ts.best_t;
       r.probe_time = ts.has_best ? ts.best_t : INF;
@@ -450,7 +503,19 @@ __global__ void __launch_bounds__(128) k_default(Bufs b, const TaskDev* tasks, i
       r.has_best = ts.has_best;
       r.best_leaf = ts.best_leaf;
       res[task] = r;
+      if (probe && ts.has_best) atomicMin(gb_bits, (unsigned long long)__double_as_longlong(ts.best_t));
+      if (b.trace) {
+        unsigned long long* rec = b.trace + 8 * (size_t)(task + (probe ? n_tasks : 0));
+        rec[0] = (unsigned long long)(clock64() - dbg_t0);
+        rec[1] = (unsigned long long)(td.leaf_end - td.leaf_begin);
+        rec[2] = (unsigned long long)dbg_steps | ((unsigned long long)(dbg_mo >> 10) << 20);
+        rec[3] = (unsigned long long)ts.sim;
+        rec[4] = (unsigned long long)dbg_seed;
+        rec[5] = (unsigned long long)dbg_sim;
+        rec[6] = (unsigned long long)dbg_gate;
+        rec[7] = (unsigned long long)dbg_rep;
+      }
     }
-    __syncwarp();
+    __syncthreads();
   }
 }

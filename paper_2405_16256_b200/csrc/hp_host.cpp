@@ -15,7 +15,7 @@ namespace {
 
 Status bad(const std::string& m) { return Status{HP_BAD_CONFIG, m}; }
 
-std::string gname(const Problem& p, int g) { return std::string(p.groups[g].name); }
+std::string gname(const Problem& p, int g) { return p.names[g]; }
 
 }  // namespace
 
@@ -28,6 +28,15 @@ Status load_problem(const hp_problem* in, Problem& p) {
     return bad("cluster: at most " + std::to_string(HP_MAX_GROUPS) + " device groups supported");
   p.groups.assign(c.groups, c.groups + c.n_groups);
   p.links.assign(c.links, c.links + c.n_links);
+  p.names.assign(p.groups.size(), std::string());
+  p.names_blob.clear();
+  p.name_off.assign(p.groups.size(), 0);
+  for (size_t g = 0; g < p.groups.size(); ++g) {
+    if (p.groups[g].name) p.names[g] = p.groups[g].name;
+    p.name_off[g] = static_cast<int>(p.names_blob.size());
+    p.names_blob += p.names[g];
+  }
+  for (size_t g = 0; g < p.groups.size(); ++g) p.groups[g].name = p.names[g].c_str();
   p.train = in->train;
 
   // ---- validate_spec(ModelSpec), types.cpp:78-91
@@ -49,7 +58,6 @@ Status load_problem(const hp_problem* in, Problem& p) {
   if (p.groups.empty()) return bad("cluster: at least one device group required");
   std::set<std::string> names;
   for (hp_group& g : p.groups) {
-    g.name[HP_NAME_LEN - 1] = 0;
     std::string n = g.name;
     if (n.empty()) return bad("cluster: group name must be non-empty");
     if (!names.insert(n).second) return bad("cluster: duplicate group name '" + n + "'");
@@ -79,7 +87,9 @@ Status load_problem(const hp_problem* in, Problem& p) {
     if (l.path == HP_CPU_STAGED && l.staging_copy_bytes_per_s <= 0)
       return bad("cluster: cpu-staged link must carry a positive staging_copy_bytes_per_s");
     if (l.scope == HP_INTRA_NODE || l.scope == HP_INTER_NODE) {
-      if (l.group_a < 0 || l.group_a >= G) return bad("cluster: link references unknown group");
+      if (l.group_a < 0 || l.group_a >= G)
+        return bad(l.group_a_name ? "cluster: link references unknown group '" + std::string(l.group_a_name) + "'"
+                                  : std::string("cluster: link references unknown group"));
       int& cnt = l.scope == HP_INTRA_NODE ? intra_count[l.group_a] : inter_count[l.group_a];
       if (++cnt > 1)
         return bad("cluster: group '" + gname(p, l.group_a) + "' has more than one " +
@@ -219,6 +229,18 @@ void enumerate(Problem& p) {
     std::vector<int> cur;
     compositions(p, pp, 0, pp, cur);
   }
+  // dp values some micro-batch candidate divides the global batch with
+  // (planner.cpp:355-357), descending; a task walks them from its dp_max
+  long long dp_cap = 1;
+  for (int g = 0; g < G; ++g)
+    dp_cap = std::max(dp_cap, static_cast<long long>(p.groups[g].node_count) * p.groups[g].devices_per_node);
+  std::vector<long long> dps;
+  for (long long dp = dp_cap; dp >= 1; --dp)
+    for (int64_t B : p.mbs)
+      if (p.train.global_batch_size % (dp * B) == 0) {
+        dps.push_back(dp);
+        break;
+      }
   for (int ti = 0; ti < static_cast<int>(p.tasks.size()); ++ti) {
     Task& t = p.tasks[ti];
     t.layout_off = static_cast<int>(p.layouts.size());
@@ -246,11 +268,34 @@ void enumerate(Problem& p) {
           if (p.groups[g].devices_per_node % d == 0) tpo[g].push_back(d);
       }
     const long long nsplit = hpc::contiguous_split_count(L, t.pp);
-    for (long long dp = dp_max; dp >= 1; --dp) {
+    // The allotment test (planner.cpp:366-379) is per group, so the leaves
+    // of a (dp, B) are the product of each group's passing tp values, in the
+    // odometer order (group 0 fastest) restricted to them.
+    std::vector<std::vector<int>> okt(G);
+    std::vector<size_t> idx(G);
+    for (long long dp : dps) {
+      if (dp > dp_max) continue;
+      bool empty = false;
+      for (int g = 0; g < G; ++g) {
+        okt[g].clear();
+        for (int tp : tpo[g]) {
+          if (t.spg[g] == 0) {
+            okt[g].push_back(tp);
+            continue;
+          }
+          long long dev = dp * tp;
+          if (dev % p.groups[g].devices_per_node != 0) continue;
+          long long nu = dev / p.groups[g].devices_per_node;
+          if (nu < 1 || nu * t.spg[g] > p.groups[g].node_count) continue;
+          okt[g].push_back(tp);
+        }
+        empty = empty || okt[g].empty();
+      }
+      if (empty) continue;
       for (int bi = 0; bi < static_cast<int>(p.mbs.size()); ++bi) {
         int64_t B = p.mbs[bi];
         if (p.train.global_batch_size % (dp * B) != 0) continue;
-        std::vector<size_t> idx(G, 0);
+        std::fill(idx.begin(), idx.end(), 0);
         for (;;) {
           LeafHost lf{};
           lf.task = ti;
@@ -258,32 +303,19 @@ void enumerate(Problem& p) {
           lf.B = B;
           lf.B_idx = bi;
           lf.M = p.train.global_batch_size / (dp * B);
-          bool ok = true;
           for (int g = 0; g < HP_MAX_GROUPS; ++g) {
-            lf.tp[g] = g < G ? tpo[g][idx[g]] : 1;
+            lf.tp[g] = g < G ? okt[g][idx[g]] : 1;
             lf.nodes[g] = 0;
           }
-          for (int g = 0; g < G && ok; ++g) {
-            if (t.spg[g] == 0) continue;
-            long long dev = dp * lf.tp[g];
-            if (dev % p.groups[g].devices_per_node != 0) {
-              ok = false;
-              break;
-            }
-            long long nu = dev / p.groups[g].devices_per_node;
-            if (nu < 1 || nu * t.spg[g] > p.groups[g].node_count) ok = false;
-            lf.nodes[g] = static_cast<int>(nu);
-          }
-          if (ok) {
-            lf.n_splits = nsplit;
-            lf.exhaustive = !p.uniform_only && nsplit <= p.limit;
-            double pm = static_cast<double>(t.pp) * static_cast<double>(lf.M);
-            lf.cost = lf.exhaustive ? pm * static_cast<double>(nsplit)
-                                    : pm * (2.0 + 12.0 * 2.0 * (t.pp - 1));
-            p.leaves.push_back(lf);
-          }
+          for (int g = 0; g < G; ++g)
+            if (t.spg[g] > 0) lf.nodes[g] = static_cast<int>(dp * lf.tp[g] / p.groups[g].devices_per_node);
+          lf.n_splits = nsplit;
+          lf.exhaustive = !p.uniform_only && nsplit <= p.limit;
+          double pm = static_cast<double>(t.pp) * static_cast<double>(lf.M);
+          lf.cost = lf.exhaustive ? pm * static_cast<double>(nsplit) : pm * (2.0 + 12.0 * 2.0 * (t.pp - 1));
+          p.leaves.push_back(lf);
           int g = 0;
-          while (g < G && ++idx[g] == tpo[g].size()) idx[g++] = 0;
+          while (g < G && ++idx[g] == okt[g].size()) idx[g++] = 0;
           if (g == G) break;
         }
       }
@@ -375,10 +407,10 @@ void fill_consts(const Problem& p, hpc::Consts& c) {
     c.budget[g] = p.groups[g].memory_bytes * p.headroom;  // planner.cpp:508
     c.link_inter[g] = p.inter[g];
     for (int h = 0; h < c.n_groups; ++h) c.link_pair[g][h] = g == h ? p.inter[g] : p.pair[g][h];
-    int n = static_cast<int>(std::strlen(p.groups[g].name));
-    std::memcpy(c.names[g], p.groups[g].name, n);
-    c.name_len[g] = n;
+    c.name_off[g] = p.name_off[g];
+    c.name_len[g] = static_cast<int>(p.names[g].size());
   }
+  c.names = p.names_blob.data();  // host copy; device users point it at a device copy
   c.n_links = static_cast<int>(p.links.size());
   c.n_B = static_cast<int>(p.mbs.size());
 }

@@ -46,7 +46,10 @@ struct LeafHost {
 struct Problem {
   // inputs
   hp_model model{};
-  std::vector<hp_group> groups;
+  std::vector<hp_group> groups;       // name pointers into `names`
+  std::vector<std::string> names;     // group names (owned copies)
+  std::string names_blob;             // names concatenated (Consts::names on the host)
+  std::vector<int> name_off;
   std::vector<hp_link> links;
   hp_train train{};
   // normalised planner (planner.cpp:585-607)

@@ -2224,6 +2224,18 @@ static hph::Status scratch(Arena& a, const char* name, size_t n, T** out) {
   return s;
 }
 
+// Consts to __constant__ memory, with the group names (encode_plan's
+// tie-break) copied to device memory first.
+static hph::Status consts_to_device(Arena& a, const hph::Problem& p, Consts& c) {
+  std::vector<char> blob(p.names_blob.begin(), p.names_blob.end());
+  char* d_names;
+  hph::Status s = upload(a, "names", blob, &d_names);
+  if (!s.ok()) return s;
+  c.names = d_names;
+  CK(cudaMemcpyToSymbolAsync(hpk::c_consts, &c, sizeof c, 0, cudaMemcpyHostToDevice, a.stream));
+  return s;
+}
+
 static size_t split_total_of(const std::vector<Leaf>& leaves) {
   size_t n = 0;
   for (const Leaf& lf : leaves) n += lf.P;
@@ -2259,9 +2271,10 @@ static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vect
   const int nL = static_cast<int>(my_leaves.size());
   Consts c;
   hph::fill_consts(p, c);
-  CK(cudaMemcpyToSymbolAsync(hpk::c_consts, &c, sizeof c, 0, cudaMemcpyHostToDevice, st));
   a.h2d_bytes = sizeof c;
   a.d2h_bytes = 0;
+  hph::Status s_;
+  if (!(s_ = consts_to_device(a, p, c)).ok()) return s_;
 
   // ---- host tables (split-independent, exact reference order)
   leaves.assign(nL, Leaf{});
@@ -2813,8 +2826,9 @@ hph::Status evaluate_plans(Arena& a, const hph::Problem& p, const hp_plan* plans
   cudaStream_t st = a.stream;
   Consts c;
   hph::fill_consts(p, c);
+  hph::Status s_;
   c.n_B = n;
-  CK(cudaMemcpyToSymbolAsync(hpk::c_consts, &c, sizeof c, 0, cudaMemcpyHostToDevice, st));
+  if (!(s_ = consts_to_device(a, p, c)).ok()) return s_;
   std::vector<Leaf> leaves(n);
   std::vector<LeafGroup> lgs;
   std::vector<uint8_t> layouts;
@@ -2891,8 +2905,9 @@ hph::Status plan_node_times(Arena& a, const hph::Problem& p, const hp_plan& pl, 
   cudaStream_t st = a.stream;
   Consts c;
   hph::fill_consts(p, c);
+  hph::Status s_;
   c.n_B = 1;
-  CK(cudaMemcpyToSymbolAsync(hpk::c_consts, &c, sizeof c, 0, cudaMemcpyHostToDevice, st));
+  if (!(s_ = consts_to_device(a, p, c)).ok()) return s_;
   const int P = pl.n_stages;
   const long long M = pl.micro_batches_per_dp_replica;
   const int64_t B = pl.micro_batch_size > 0 ? pl.micro_batch_size : p.train.micro_batch_size;
@@ -3082,38 +3097,71 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   int* d_tbest;
   if (!(s = scratch(a, "d_tres", nT, &d_res)).ok()) return s;
   if (!(s = scratch(a, "d_tbest", best_total, &d_tbest)).ok()) return s;
-  const int threads = 128;
-  const int warps = std::min(nT, a.sm_count * 16);
-  const int blocks = (warps * 32 + threads - 1) / threads;
-  const size_t nw = (size_t)blocks * (threads / 32);
+  // Tasks run longest expected first (sum over leaves of P*M: the cost of a
+  // simulation, plus the gating of the leaf); the order is free, since the
+  // reduction (k_final_tasks) and the log are keyed by task.
+  std::vector<int> order(nT);
+  std::vector<double> est(nT, 0.0);
+  int max_leaves = 1;
+  for (int k = 0; k < nT; ++k) {
+    order[k] = k;
+    for (int j = tasks[k].leaf_begin; j < tasks[k].leaf_end; ++j)
+      est[k] += (double)leaves[j].P * (double)leaves[j].M + 64.0 * leaves[j].P * leaves[j].P;
+    max_leaves = std::max(max_leaves, tasks[k].leaf_end - tasks[k].leaf_begin);
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return est[x] > est[y]; });
+  int* d_order;
+  if (!(s = upload(a, "d_order", order, &d_order)).ok()) return s;
+  const int threads = hpk::DEF_THREADS;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hpk::k_default, threads, 0);
+  const int blocks = std::min(nT, a.sm_count * std::max(1, per_sm));
   hpk::DefScratch sc;
   sc.CH = hpk::DEF_CH;
-  if (!(s = scratch(a, "sc_ids", nw * sc.CH, &sc.ids)).ok()) return s;
-  if (!(s = scratch(a, "sc_lower", nw * sc.CH, &sc.lower)).ok()) return s;
-  if (!(s = scratch(a, "sc_times", nw * sc.CH, &sc.times)).ok()) return s;
-  if (!(s = scratch(a, "sc_flag", nw * sc.CH, &sc.flag)).ok()) return s;
-  if (!(s = scratch(a, "sc_dec", nw * sc.CH, &sc.dec)).ok()) return s;
+  sc.SC = max_leaves;
+  const size_t nb = (size_t)blocks;
+  if (!(s = scratch(a, "sc_ids", nb * sc.CH, &sc.ids)).ok()) return s;
+  if (!(s = scratch(a, "sc_lower", nb * sc.CH, &sc.lower)).ok()) return s;
+  if (!(s = scratch(a, "sc_times", nb * sc.CH, &sc.times)).ok()) return s;
+  if (!(s = scratch(a, "sc_flag", nb * sc.CH, &sc.flag)).ok()) return s;
+  if (!(s = scratch(a, "sc_dec", nb * sc.CH, &sc.dec)).ok()) return s;
+  if (!(s = scratch(a, "sc_sflag", nb * 2 * sc.SC, &sc.sflag)).ok()) return s;
+  if (!(s = scratch(a, "sc_slow", nb * 2 * sc.SC, &sc.slow)).ok()) return s;
   int* d_next;
   if (!(s = scratch(a, "d_next", 4, &d_next)).ok()) return s;
   unsigned long long* d_ops;
   if (!(s = scratch(a, "ops", 4, &d_ops)).ok()) return s;
   CK(cudaMemsetAsync(d_ops, 0, 4 * sizeof(unsigned long long), st));
   b.ops = d_ops;
+  // the global bound as the bit pattern of a non-negative double: the probe
+  // pass folds every task's first simulated seed into it with atomicMin, the
+  // main pass reads it on the device (no host round trip in between)
+  unsigned long long* d_gb;
+  if (!(s = scratch(a, "d_gb", 1, &d_gb)).ok()) return s;
+  {
+    double g0 = have_bound ? bound : std::numeric_limits<double>::infinity();
+    CK(cudaMemcpyAsync(d_gb, &g0, sizeof g0, cudaMemcpyHostToDevice, st));
+  }
 
+  const char* dbg_tasks = std::getenv("HP_DEBUG_TASKS");  // per-task cycle records (diagnostics)
+  if (dbg_tasks) {
+    if (!(s = scratch(a, "dbg_tasks", 16 * (size_t)nT, &b.trace)).ok()) return s;
+    CK(cudaMemsetAsync(b.trace, 0, sizeof(unsigned long long) * 16 * nT, st));
+  }
   if (!have_bound) {
     CK(cudaMemsetAsync(d_next, 0, sizeof(int), st));
-    hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, nT, d_next, d_res, d_tbest, sc, 0.0, 1,
+    hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, d_order, nT, d_next, d_res, d_tbest, sc, d_gb, 1,
                                                p.uniform_only ? 1 : 0);
     out.launches++;
     out.eval_launches++;
-    std::vector<hpk::TaskRes> pr(nT);
-    CK(cudaMemcpyAsync(pr.data(), d_res, sizeof(hpk::TaskRes) * nT, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    a.d2h_bytes += sizeof(hpk::TaskRes) * nT;
-    double gb = std::numeric_limits<double>::infinity();
-    for (const auto& r : pr) gb = std::min(gb, r.probe_time);
-    out.global_bound = gb;
-    if (probe_only) return hph::Status{};
+    if (probe_only) {
+      double gb = 0.0;
+      CK(cudaMemcpyAsync(&gb, d_gb, sizeof gb, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      a.d2h_bytes += sizeof gb;
+      out.global_bound = gb;
+      return hph::Status{};
+    }
   }
   CK(cudaMemsetAsync(d_next, 0, sizeof(int), st));
   if (a.log.on) {
@@ -3126,8 +3174,8 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
     a.event_pair(&e0, &e1);
     cudaEventRecord(e0, st);
   }
-  hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, nT, d_next, d_res, d_tbest, sc,
-                                             out.global_bound, 0, p.uniform_only ? 1 : 0);
+  hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, d_order, nT, d_next, d_res, d_tbest, sc, d_gb, 0,
+                                             p.uniform_only ? 1 : 0);
   if (a.time_evals) cudaEventRecord(e1, st);
   out.launches++;
   out.eval_launches++;
@@ -3144,9 +3192,23 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   CK(cudaMemcpyAsync(&bt, d_bt, sizeof bt, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(counts, d_counts, sizeof counts, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(ops, d_ops, sizeof ops, cudaMemcpyDeviceToHost, st));
+  if (!have_bound) CK(cudaMemcpyAsync(&out.global_bound, d_gb, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (a.time_evals) out.eval_ms = a.drain_events();
   if (a.log.on && !(s = log_collect(a, b.log, tasks.size())).ok()) return s;
+  if (dbg_tasks) {
+    std::vector<unsigned long long> rec(16 * (size_t)nT);
+    CK(cudaMemcpy(rec.data(), b.trace, sizeof(unsigned long long) * rec.size(), cudaMemcpyDeviceToHost));
+    if (FILE* fp = std::fopen(dbg_tasks, "wb")) {
+      for (int k = 0; k < nT; ++k) {
+        std::fprintf(fp, "%d %d", task_ids[k], tasks[k].pp);
+        for (int q = 0; q < 8; ++q) std::fprintf(fp, " %llu", rec[8 * (size_t)k + q]);
+        for (int q = 0; q < 8; ++q) std::fprintf(fp, " %llu", rec[8 * ((size_t)nT + k) + q]);
+        std::fprintf(fp, "\n");
+      }
+      std::fclose(fp);
+    }
+  }
   out.eval_fp64_ops = static_cast<double>(ops[0]);
   out.dev_simulated = static_cast<long long>(ops[1]);
   out.dev_aborted = static_cast<long long>(ops[2]);

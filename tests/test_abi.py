@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     for fn in decl:
         assert fn in syms, fn
         assert hasattr(l, fn)
-    assert l.hp_abi_version() == 2
+    assert l.hp_abi_version() == 3
 
 
 def test_struct_layout_matches_header(tmp_path):
@@ -85,6 +85,11 @@ BAD = [
     ("planner", lambda d: d["planner"].__setitem__("pipeline_degrees", [0, 2]), "planner: pipeline degrees must be >= 1"),
     ("planner", lambda d: d["planner"].__setitem__("stage_order_beam_width", -1),
      "planner: stage_order_beam_width must be >= 0"),
+    # the unknown name itself is in the message (types.cpp:126)
+    ("cluster", lambda d: d["cluster"]["links"][0]["endpoints"].__setitem__("group", "nosuch"),
+     "cluster: link references unknown group 'nosuch'"),
+    ("cluster", lambda d: d["cluster"]["links"][4]["endpoints"].__setitem__("group_b", "nosuch"),
+     "cluster: inter-group link references undeclared group"),
 ]
 
 
@@ -99,6 +104,33 @@ def test_validation_messages(doc, mutate, msg):
     if ref.available():  # the reference raises the same ConfigError text
         r = ref.search(d)
         assert r["status"] == 1 and r["error"] == msg
+
+
+def test_long_names_and_many_groups():
+    """Group names of any length and up to HP_MAX_GROUPS groups pass the
+    boundary; a longer list is rejected with a ConfigError naming the cap."""
+    d = copy.deepcopy(configs.config("C0"))
+    long_name = "accelerator-with-a-very-long-vendor-specific-name-0123456789"
+    for l in d["cluster"]["links"]:
+        ep = l["endpoints"]
+        for k in ("group", "group_a", "group_b"):
+            if ep.get(k) == "amd":
+                ep[k] = long_name
+    d["cluster"]["groups"][0]["name"] = long_name
+    assert validate(d)[0] == abi.HP_OK
+    p = abi.Problem(d)
+    pl = p.plan_from_doc({"schedule": "1f1b", "micro_batches_per_dp_replica": 4, "micro_batch_size": 1,
+                          "stages": [{"layer_range": [0, 80], "group": long_name, "nodes_used": 1,
+                                      "tp_degree": 8, "dp_degree": 1}]})
+    assert abi.encode_plan(p.group_names, pl).startswith("1f1b|4|1|" + long_name + ":0-80")
+    from paper_2405_16256_b200 import configs as cf
+    many = [cf.group(f"g{k}", cf.GROUP_PRESETS["amd"], 1, 8) for k in range(abi.HP_MAX_GROUPS)]
+    d2 = copy.deepcopy(configs.config("C0"))
+    d2["cluster"] = cf.cluster_doc(many)
+    assert validate(d2)[0] == abi.HP_OK
+    d2["cluster"] = cf.cluster_doc(many + [cf.group("extra", cf.GROUP_PRESETS["amd"], 1, 8)])
+    with pytest.raises(abi.ConfigError, match="at most 16 device groups"):
+        validate(d2)
 
 
 def test_valid_config_validates():
