@@ -221,14 +221,48 @@ HPD void split_layers(int total, const double* w, int parts, int* counts, double
     assigned += counts[i];
   }
   int remainder = total - assigned;
-  // std::stable_sort by fraction descending == stable insertion sort
-  for (int i = 0; i < parts; ++i) {
-    int j = i;
-    while (j > 0 && frac[order[j - 1]] < frac[i]) {
-      order[j] = order[j - 1];
-      --j;
+  // std::stable_sort by fraction descending. Stages of one device group
+  // (and tp) share a weight, so the fractions take few distinct values:
+  // emit the indices of each distinct value, largest first, in index order
+  // (O(parts x distinct)); many distinct values fall back to a stable
+  // insertion sort. Both give exactly std::stable_sort's order.
+  constexpr int kDistinct = 16;
+  double dv[kDistinct];
+  int nd = 0;
+  for (int i = 0; i < parts && nd <= kDistinct; ++i) {
+    int k = 0;
+    while (k < nd && !(dv[k] == frac[i])) ++k;
+    if (k == nd) {
+      if (nd == kDistinct) {
+        nd = kDistinct + 1;
+        break;
+      }
+      dv[nd++] = frac[i];
     }
-    order[j] = i;
+  }
+  if (nd <= kDistinct) {
+    for (int a = 1; a < nd; ++a) {  // distinct values, descending
+      const double x = dv[a];
+      int k = a;
+      while (k > 0 && dv[k - 1] < x) {
+        dv[k] = dv[k - 1];
+        --k;
+      }
+      dv[k] = x;
+    }
+    int o = 0;
+    for (int k = 0; k < nd; ++k)
+      for (int i = 0; i < parts; ++i)
+        if (frac[i] == dv[k]) order[o++] = i;
+  } else {
+    for (int i = 0; i < parts; ++i) {
+      int j = i;
+      while (j > 0 && frac[order[j - 1]] < frac[i]) {
+        order[j] = order[j - 1];
+        --j;
+      }
+      order[j] = i;
+    }
   }
   for (int r = 0; r < remainder; ++r) ++counts[order[r % parts]];
   for (int i = 0; i < parts; ++i) {

@@ -38,9 +38,21 @@ struct DefScratch {
   unsigned char* flag;  // bit0 valid, bit1 mem_ok, bit2 old
   double* dec;          // per-slot decision of a hill step (time or -1)
   int CH;
-  unsigned char* sflag; // seeds: flag bits, bit3 = proportional equals uniform (memo hit)
-  double* slow;         // seeds: lower bounds
-  int SC;
+};
+
+// Per-leaf seed state (indexed by leaf; computed once per search, by the
+// probe pass when there is one, else by the main pass).
+struct DefSeeds {
+  unsigned char* flag;  // [2*leaf + s]: gate bits, bit3 = proportional equals uniform (memo hit)
+  double* low;          // [2*leaf + s]: lower bounds
+  unsigned char* done;  // [2*leaf + s]: tseed holds its simulated time already
+  // exhaustive leaves: compositions the memory gate prunes, feasible ones,
+  // and the least lower bound among the feasible (seeds, memo hits,
+  // excluded) — a leaf whose least bound is above the incumbent is decided
+  // without being enumerated again
+  long long* xmem;
+  long long* xfeas;
+  double* xmin;
 };
 
 constexpr int DEF_CH = 1024;
@@ -168,7 +180,8 @@ __device__ inline void simulate_list(const Bufs& b, int li, int kind, const long
 // patterns of non-negative doubles); otherwise *gb_bits is the global bound.
 __global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs b, const TaskDev* tasks, const int* order, int n_tasks,
                                                         int* next_task, TaskRes* res, int* tbest_rows, DefScratch sc,
-                                                        unsigned long long* gb_bits, int probe, int uniform_only) {
+                                                        DefSeeds sd, int seeds_ready, unsigned long long* gb_bits,
+                                                        int probe, int uniform_only) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   long long* ids = sc.ids + (size_t)blockIdx.x * sc.CH;  // global: the evaluators read it
@@ -177,8 +190,6 @@ __global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs b, const TaskDev* 
   __shared__ double lower[DEF_CH];
   __shared__ double dec[DEF_CH];
   __shared__ unsigned char flag[DEF_CH];
-  unsigned char* sflag = sc.sflag + (size_t)blockIdx.x * 2 * sc.SC;
-  double* slow = sc.slow + (size_t)blockIdx.x * 2 * sc.SC;
   Bufs bx = b;
   bx.xbuf = sc.times;
   const int xbase = blockIdx.x * sc.CH;
@@ -213,7 +224,7 @@ __global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs b, const TaskDev* 
 
     // ---- seeds of every leaf and their gates (incumbent-free)
     const int nl = td.leaf_end - td.leaf_begin;
-    for (int j = tid; j < nl; j += DEF_THREADS) {
+    for (int j = seeds_ready ? nl : tid; j < nl; j += DEF_THREADS) {
       const int li = td.leaf_begin + j;
       const Leaf lf = b.leaves[li];
       const LeafGroup* lg = b.lg + lf.lg_off;
@@ -225,14 +236,39 @@ __global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs b, const TaskDev* 
       int ord[HP_MAX_STAGES];
       seed_splits(c_consts, lf, lg, slots, uni, prop, w, frac, ord);
       double lo = 0.0;
-      sflag[2 * j] = cand_gate(c_consts, lf, lg, slots, hop, uni, &lo);
-      slow[2 * j] = lo;
+      sd.flag[2 * li] = cand_gate(c_consts, lf, lg, slots, hop, uni, &lo);
+      sd.low[2 * li] = lo;
       if (same_split(uni, prop, lf.P)) {
-        sflag[2 * j + 1] = 8;
-        slow[2 * j + 1] = 0.0;
+        sd.flag[2 * li + 1] = 8;
+        sd.low[2 * li + 1] = 0.0;
       } else {
-        sflag[2 * j + 1] = cand_gate(c_consts, lf, lg, slots, hop, prop, &lo);
-        slow[2 * j + 1] = lo;
+        sd.flag[2 * li + 1] = cand_gate(c_consts, lf, lg, slots, hop, prop, &lo);
+        sd.low[2 * li + 1] = lo;
+      }
+      sd.done[2 * li] = sd.done[2 * li + 1] = 0;
+      if (lf.mode == 1 && !uniform_only) {
+        const long long total = contiguous_split_count(c_consts.L, lf.P);
+        const long long ru = rank_composition(uni, c_consts.L, lf.P);
+        const long long rp = rank_composition(prop, c_consts.L, lf.P);
+        int comp[HP_MAX_STAGES];
+        long long nmem = 0, nfeas = 0;
+        double mn = INF;
+        unrank_composition(0, c_consts.L, lf.P, comp);
+        for (long long r = 0; r < total; ++r) {
+          if (r) next_composition(comp, lf.P);
+          if (r == ru || r == rp) continue;
+          double l;
+          const unsigned char f = cand_gate(c_consts, lf, lg, slots, hop, comp, &l);
+          if (!(f & 2)) {
+            ++nmem;
+          } else {
+            ++nfeas;
+            if (l < mn) mn = l;
+          }
+        }
+        sd.xmem[li] = nmem;
+        sd.xfeas[li] = nfeas;
+        sd.xmin[li] = mn;
       }
     }
     __syncthreads();
@@ -255,9 +291,12 @@ __global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs b, const TaskDev* 
         const double inc0 = incumbent(ts, gb);
         int n = 0;
         for (int s = 0; s < nseed; ++s) {
-          const unsigned char f = sflag[2 * j + s];
-          if (f & 8) continue;
-          if ((f & 2) && !(pruning && inc0 < INF && slow[2 * j + s] > inc0)) ids[n++] = s;
+          const unsigned char f = sd.flag[2 * li + s];
+          if ((f & 8) || sd.done[2 * li + s]) continue;
+          if ((f & 2) && !(pruning && inc0 < INF && sd.low[2 * li + s] > inc0)) {
+            ids[n++] = s;
+            sd.done[2 * li + s] = 1;  // (the time lands in tseed below)
+          }
         }
         s_cnt = n;
       }
@@ -269,7 +308,7 @@ __global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs b, const TaskDev* 
       if (tid == 0) {
         double dseed[2] = {-1.0, -1.0};
         for (int s = 0; s < nseed; ++s) {
-          const unsigned char f = sflag[2 * j + s];
+          const unsigned char f = sd.flag[2 * li + s];
           if (f & 8) {  // memo hit (planner.cpp:425-432)
             dseed[1] = dseed[0];
             continue;
@@ -277,7 +316,7 @@ __global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs b, const TaskDev* 
           const double inc = incumbent(ts, gb);
           if (!(f & 2)) {
             ts.pmem++;
-          } else if (pruning && inc < INF && slow[2 * j + s] > inc) {
+          } else if (pruning && inc < INF && sd.low[2 * li + s] > inc) {
             ts.pbound++;
           } else {
             const double t = b.tseed[2 * li + s];
@@ -304,6 +343,19 @@ __global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs b, const TaskDev* 
 
       if (lf.mode == 1) {
         // ---- exhaustive, in rank order (planner.cpp:454-459)
+        if (tid == 0) {
+          // every feasible composition's bound above the incumbent: all
+          // bound-pruned, nothing simulated, no need to enumerate again
+          const double inc = incumbent(ts, gb);
+          const double mn = sd.xmin[li];
+          s_stop = pruning && inc < INF && mn > inc;
+          if (s_stop) {
+            ts.pmem += sd.xmem[li];
+            ts.pbound += sd.xfeas[li];
+          }
+        }
+        __syncthreads();
+        if (s_stop) continue;
         const long long total = contiguous_split_count(c_consts.L, P);
         long long ru = 0, rp = 0;
         ru = rank_composition(uni, c_consts.L, P);

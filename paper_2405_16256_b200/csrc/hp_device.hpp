@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <map>
 #include <string>
 #include <vector>
@@ -66,6 +67,30 @@ struct Arena {
 
   LogRaw log;
 
+  // Pinned staging for host->device table uploads (a pageable cudaMemcpy
+  // stages through a driver buffer at a fraction of the bandwidth). A
+  // bump allocator, reset per search; growing it first drains the stream.
+  char* pinned = nullptr;
+  size_t pinned_cap = 0, pinned_used = 0;
+  char* stage(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (pinned_used + bytes > pinned_cap) {
+      cudaStreamSynchronize(stream);
+      if (pinned) cudaFreeHost(pinned);
+      pinned = nullptr;
+      size_t want = std::max(pinned_cap * 2, pinned_used + bytes + (size_t(8) << 20));
+      if (cudaHostAlloc(reinterpret_cast<void**>(&pinned), want, cudaHostAllocDefault) != cudaSuccess) {
+        pinned_cap = pinned_used = 0;
+        return nullptr;
+      }
+      pinned_cap = want;
+      pinned_used = 0;
+    }
+    char* p = pinned + pinned_used;
+    pinned_used += bytes;
+    return p;
+  }
+
   // optional per-launch timing of the evaluator kernels (bench roofline)
   bool time_evals = false;
   int shard_count = 1;  // shards of the whole search (climb scheduling policy only)
@@ -111,6 +136,9 @@ struct Arena {
   }
 
   void release() {
+    if (pinned) cudaFreeHost(pinned);
+    pinned = nullptr;
+    pinned_cap = pinned_used = 0;
     for (auto& kv : bufs)
       if (kv.second.first) cudaFree(kv.second.first);
     bufs.clear();

@@ -34,6 +34,7 @@
 #include <limits>
 #include <string>
 #include <type_traits>
+#include <unordered_map>
 #include <vector>
 
 #include "hp_device.hpp"
@@ -2210,7 +2211,15 @@ static hph::Status upload(Arena& a, const char* name, const std::vector<T>& v, T
   void* p = nullptr;
   hph::Status s = a.get(name, std::max<size_t>(1, v.size()) * sizeof(T), &p);
   if (!s.ok()) return s;
-  if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, a.stream));
+  if (!v.empty()) {
+    const size_t nb = v.size() * sizeof(T);
+    if (char* h = a.stage(nb)) {
+      std::memcpy(h, v.data(), nb);
+      CK(cudaMemcpyAsync(p, h, nb, cudaMemcpyHostToDevice, a.stream));
+    } else {
+      CK(cudaMemcpyAsync(p, v.data(), nb, cudaMemcpyHostToDevice, a.stream));
+    }
+  }
   a.h2d_bytes += static_cast<double>(v.size() * sizeof(T));
   *out = static_cast<T*>(p);
   return s;
@@ -2227,6 +2236,9 @@ static hph::Status scratch(Arena& a, const char* name, size_t n, T** out) {
 // Consts to __constant__ memory, with the group names (encode_plan's
 // tie-break) copied to device memory first.
 static hph::Status consts_to_device(Arena& a, const hph::Problem& p, Consts& c) {
+  // a new search / evaluation: the previous one's staged copies are done
+  // (every entry point synchronises its stream before returning)
+  a.pinned_used = 0;
   std::vector<char> blob(p.names_blob.begin(), p.names_blob.end());
   char* d_names;
   hph::Status s = upload(a, "names", blob, &d_names);
@@ -2278,19 +2290,44 @@ static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vect
 
   // ---- host tables (split-independent, exact reference order)
   leaves.assign(nL, Leaf{});
-  std::vector<LeafGroup> lgs((size_t)nL * G);
+  std::vector<LeafGroup> lgs;
   std::vector<int> hist_off(nL), nb_off(nL);
   std::vector<double> hop = hph::hop_table(p);
   int split_total = 0, hist_total = 0, nb_total = 0;
   hill_ids.clear();
   exh_ids.clear();
+  // A leaf's G cost rows depend only on (dp, B, tp and nodes per group), so
+  // leaves share them: one copy per distinct tuple (C3: ~600 for 63k leaves)
+  struct KeyHash {
+    size_t operator()(const std::vector<long long>& v) const {
+      unsigned long long h = 1469598103934665603ULL;  // FNV-1a over the values
+      for (long long x : v) h = (h ^ static_cast<unsigned long long>(x)) * 1099511628211ULL;
+      return static_cast<size_t>(h);
+    }
+  };
+  std::unordered_map<std::vector<long long>, int, KeyHash> row_of;
+  row_of.reserve(4096);
+  std::vector<long long> key(3 + 2 * G);
   for (int k = 0; k < nL; ++k) {
     Leaf& lf = leaves[k];
     lf = hph::device_leaf(p, my_leaves[k]);
     lf.split_off = split_total;
-    lf.lg_off = k * G;
     split_total += lf.P;
-    hph::leaf_rows(p, my_leaves[k], &lgs[(size_t)k * G]);
+    const hph::LeafHost& h = p.leaves[my_leaves[k]];
+    key[0] = h.dp;
+    key[1] = h.B_idx;
+    key[2] = h.B;
+    for (int g = 0; g < G; ++g) {
+      key[3 + 2 * g] = h.tp[g];
+      key[4 + 2 * g] = h.nodes[g];
+    }
+    auto it = row_of.find(key);
+    if (it == row_of.end()) {
+      it = row_of.emplace(key, static_cast<int>(lgs.size())).first;
+      lgs.resize(lgs.size() + G);
+      hph::leaf_rows(p, my_leaves[k], &lgs[lgs.size() - G]);
+    }
+    lf.lg_off = it->second;
     hist_off[k] = hist_total;
     nb_off[k] = nb_total;
     if (lf.mode == 0) {
@@ -3102,12 +3139,10 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   // reduction (k_final_tasks) and the log are keyed by task.
   std::vector<int> order(nT);
   std::vector<double> est(nT, 0.0);
-  int max_leaves = 1;
   for (int k = 0; k < nT; ++k) {
     order[k] = k;
     for (int j = tasks[k].leaf_begin; j < tasks[k].leaf_end; ++j)
       est[k] += (double)leaves[j].P * (double)leaves[j].M + 64.0 * leaves[j].P * leaves[j].P;
-    max_leaves = std::max(max_leaves, tasks[k].leaf_end - tasks[k].leaf_begin);
   }
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return est[x] > est[y]; });
   int* d_order;
@@ -3118,15 +3153,20 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   const int blocks = std::min(nT, a.sm_count * std::max(1, per_sm));
   hpk::DefScratch sc;
   sc.CH = hpk::DEF_CH;
-  sc.SC = max_leaves;
   const size_t nb = (size_t)blocks;
+  const size_t nl = std::max<size_t>(1, my_leaves.size());
+  hpk::DefSeeds sd;
+  if (!(s = scratch(a, "sd_flag", 2 * nl, &sd.flag)).ok()) return s;
+  if (!(s = scratch(a, "sd_low", 2 * nl, &sd.low)).ok()) return s;
+  if (!(s = scratch(a, "sd_done", 2 * nl, &sd.done)).ok()) return s;
+  if (!(s = scratch(a, "sd_xmem", nl, &sd.xmem)).ok()) return s;
+  if (!(s = scratch(a, "sd_xfeas", nl, &sd.xfeas)).ok()) return s;
+  if (!(s = scratch(a, "sd_xmin", nl, &sd.xmin)).ok()) return s;
   if (!(s = scratch(a, "sc_ids", nb * sc.CH, &sc.ids)).ok()) return s;
   if (!(s = scratch(a, "sc_lower", nb * sc.CH, &sc.lower)).ok()) return s;
   if (!(s = scratch(a, "sc_times", nb * sc.CH, &sc.times)).ok()) return s;
   if (!(s = scratch(a, "sc_flag", nb * sc.CH, &sc.flag)).ok()) return s;
   if (!(s = scratch(a, "sc_dec", nb * sc.CH, &sc.dec)).ok()) return s;
-  if (!(s = scratch(a, "sc_sflag", nb * 2 * sc.SC, &sc.sflag)).ok()) return s;
-  if (!(s = scratch(a, "sc_slow", nb * 2 * sc.SC, &sc.slow)).ok()) return s;
   int* d_next;
   if (!(s = scratch(a, "d_next", 4, &d_next)).ok()) return s;
   unsigned long long* d_ops;
@@ -3150,8 +3190,8 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   }
   if (!have_bound) {
     CK(cudaMemsetAsync(d_next, 0, sizeof(int), st));
-    hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, d_order, nT, d_next, d_res, d_tbest, sc, d_gb, 1,
-                                               p.uniform_only ? 1 : 0);
+    hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, d_order, nT, d_next, d_res, d_tbest, sc, sd, 0, d_gb,
+                                               1, p.uniform_only ? 1 : 0);
     out.launches++;
     out.eval_launches++;
     if (probe_only) {
@@ -3174,8 +3214,9 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
     a.event_pair(&e0, &e1);
     cudaEventRecord(e0, st);
   }
-  hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, d_order, nT, d_next, d_res, d_tbest, sc, d_gb, 0,
-                                             p.uniform_only ? 1 : 0);
+  // the probe pass computed every leaf's seeds (and simulated some)
+  hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, d_order, nT, d_next, d_res, d_tbest, sc, sd,
+                                             have_bound ? 0 : 1, d_gb, 0, p.uniform_only ? 1 : 0);
   if (a.time_evals) cudaEventRecord(e1, st);
   out.launches++;
   out.eval_launches++;

@@ -53,6 +53,7 @@ def build_emu():
     lib.emu_search.argtypes = [C.POINTER(abi.hp_problem), C.POINTER(abi.hp_result)]
     lib.emu_search_shard.argtypes = [C.POINTER(abi.hp_problem), C.c_int, C.c_int, C.POINTER(abi.hp_result)]
     lib.emu_screen_stats.argtypes = [C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), C.c_int]
+    lib.emu_split_layers.argtypes = [C.c_int, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_int)]
     return lib
 
 

@@ -225,3 +225,10 @@ extern "C" long long emu_check_bounded(int L, int P, const int* caps) {
   if (have_iter && next_bounded(want.data(), P, caps, sufcap.data())) return -1;
   return n == F ? n : -1;
 }
+
+// split_layers (hp_core.cuh) on positive weights with total >= parts.
+extern "C" void emu_split_layers(int total, const double* w, int parts, int* out) {
+  std::vector<double> frac(parts);
+  std::vector<int> order(parts);
+  split_layers(total, w, parts, out, frac.data(), order.data());
+}

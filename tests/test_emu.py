@@ -8,6 +8,8 @@ from __future__ import annotations
 import ctypes as C
 import struct
 
+import pytest
+
 from paper_2405_16256_b200 import abi
 
 
@@ -71,3 +73,31 @@ def test_emu_shards_partition_the_leaves(search_cases, emu):
             assert hexbits(red.best_time_s) == case["iteration_bits"]
             want = abi.encode_plan(p.group_names, p.plan_from_doc(case["plan"]))
             assert abi.encode_plan(p.group_names, red.best_plan) == want
+
+
+def test_device_split_layers_matches_reference(emu):
+    """hp_core.cuh split_layers (the device apportionment of k_seeds /
+    k_default, planner.cpp:42-84) equals the compiled reference on random
+    weights: few distinct values (the grouped stable-sort path: stages of a
+    device group share a weight) and many (the insertion-sort fallback)."""
+    import ctypes as C
+    import random
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    rng = random.Random(17)
+    for k in range(3000):
+        parts = rng.choice([1, 2, 3, 5, 8, 12, 24, 40, 80, 96, 160])
+        total = parts + rng.randrange(0, 400)
+        if k % 3 == 0:
+            w = [rng.uniform(0.1, 10.0) for _ in range(parts)]
+        else:
+            vals = [rng.choice([36.0, 94.0, 147.0 * 0.327 * 8, 383 * 0.245 * 4, 1.0]) for _ in range(rng.randint(1, 3))]
+            w = [rng.choice(vals) for _ in range(parts)]
+            if k % 2:
+                s = sum(w)
+                w = [x / s for x in w]  # stage_weights normalises (planner.cpp:94-103)
+        arr = (C.c_double * parts)(*w)
+        out = (C.c_int * parts)()
+        emu.emu_split_layers(total, arr, parts, out)
+        assert list(out) == ref.split_layers(total, w), (total, w)
