@@ -91,6 +91,7 @@ hp_status hp_create(hp_ctx** out, int device) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->arena.stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
+  if (e == cudaSuccess && !hpd::reserve_local_memory().ok()) e = cudaErrorMemoryAllocation;
   if (e != cudaSuccess) {
     delete ctx;
     return HP_CUDA;

@@ -174,6 +174,10 @@ struct SearchOut {
   double h2d_bytes = 0.0, d2h_bytes = 0.0;
 };
 
+// Reserves the kernels' per-thread stack on the current device (once per
+// context, hp_create).
+hph::Status reserve_local_memory();
+
 // Full strategy sweep (time_bound_pruning = false) over `my_leaves`.
 hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>& my_leaves,
                         SearchOut& out);

@@ -875,6 +875,8 @@ struct AsyncQ {
                                 // whose warps 4-7 exit: critical items run alone on their
                                 // sub-partitions (see k_hill_async)
   int r1_thr;                   // see pop_item (0: every warp serves ring 1)
+  int r0_thr;                   // < 0: ring 0 only on lead warps; else also on the others while
+                                // its backlog exceeds r0_thr
 };
 
 __device__ __forceinline__ int leaf_class(const Leaf& lf) { return eval_class(lf.P, lf.M, lf.sched == 0); }
@@ -1504,7 +1506,7 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int 
   unsigned long long seen = *(volatile unsigned long long*)q.progress;
   for (;;) {
     // 1) a held ticket that has been filled meanwhile
-    for (int lv = lv0; lv < kRings; ++lv) {
+    for (int lv = 0; lv < kRings; ++lv) {
       if (tk[lv] < 0) continue;
       const int r = try_slot(q, lv, (unsigned long long)tk[lv], w);
       if (r < 0) {
@@ -1520,7 +1522,12 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int 
     // ticket that is being filled (the producer bumps the tail before it
     // writes the slot) is waited for rather than a lower ring started
     bool held = false;
-    for (int lv = lv0; lv < kRings && !held; ++lv) {
+    int lv_start = lv0;
+    if (lv0 == 1 && q.r0_thr >= 0 &&
+        *(volatile unsigned long long*)q.tail[0] - *(volatile unsigned long long*)q.head[0] >
+            (unsigned long long)q.r0_thr)
+      lv_start = 0;  // a deep critical backlog: help it
+    for (int lv = lv_start; lv < kRings && !held; ++lv) {
       const unsigned long long tl = *(volatile unsigned long long*)q.tail[lv];
       const unsigned long long hd = *(volatile unsigned long long*)q.head[lv];
       // (r1_thr > 0: a non-lead warp takes a long-climber item only from a
@@ -1569,6 +1576,9 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int 
 #endif
 // threads per block of the climb kernel (tuning: 384 = 12 warps per SM at
 // <= 168 registers)
+#ifndef HP_CLIMB_K8
+#define HP_CLIMB_K8 1  // tuning: 0 leaves the K = 8 evaluators out of the climb kernel
+#endif
 #ifndef HP_ASYNC_MAXT
 #define HP_ASYNC_MAXT 256
 #endif
@@ -1611,11 +1621,17 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
       case 0: eval_item_call<2, true>(b, w, lane); break;
       case 1: eval_item_call<4, true>(b, w, lane); break;
       case 2: eval_item_call<6, true>(b, w, lane); break;
+#if HP_CLIMB_K8
       case 3: eval_item_call<8, true>(b, w, lane); break;
+#endif
       case 4: eval_item_call<1, false>(b, w, lane); break;
       case 5: eval_item_call<2, false>(b, w, lane); break;
       case 6: eval_item_call<3, false>(b, w, lane); break;
+#if HP_CLIMB_K8
       default: eval_item_call<8, false>(b, w, lane); break;
+#else
+      default: break;  // (tuning builds without the K = 8 evaluators)
+#endif
     }
     __syncwarp();
     if (tr_item && lane == 0) trace_event(b, 2, w.leaf, b.leaves[w.leaf], w.first);
@@ -2233,6 +2249,27 @@ static hph::Status scratch(Arena& a, const char* name, size_t n, T** out) {
   return s;
 }
 
+// The per-thread stack (local memory) the kernels need, reserved once per
+// context: without it the driver grows the device's local-memory pool at
+// the first launch that needs more and may shrink it again afterwards, a
+// device-wide reallocation on the critical path of every search (measured
+// as a ~16 ms gap before the climb kernel's first item).
+hph::Status reserve_local_memory() {
+  size_t want = 0;
+  const void* fns[] = {reinterpret_cast<const void*>(hpk::k_hill_async),
+                       reinterpret_cast<const void*>(hpk::k_default),
+                       reinterpret_cast<const void*>(hpk::k_async_seed),
+                       reinterpret_cast<const void*>(hpk::k_seeds)};
+  for (const void* f : fns) {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, f) == cudaSuccess) want = std::max(want, fa.localSizeBytes);
+  }
+  size_t cur = 0;
+  CK(cudaDeviceGetLimit(&cur, cudaLimitStackSize));
+  if (cur < want) CK(cudaDeviceSetLimit(cudaLimitStackSize, want));
+  return hph::Status{};
+}
+
 // Consts to __constant__ memory, with the group names (encode_plan's
 // tie-break) copied to device memory first.
 static hph::Status consts_to_device(Arena& a, const hph::Problem& p, Consts& c) {
@@ -2564,6 +2601,8 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     q.hi_levels = 1LL << 17;
     q.r1_thr = -1;  // set below from the grid (one item per SM of backlog)
     if (const char* e = std::getenv("HP_R1_THR")) q.r1_thr = std::max(0, std::atoi(e));  // tuning
+    q.r0_thr = -1;
+    if (const char* e = std::getenv("HP_R0_THR")) q.r0_thr = std::atoi(e);  // tuning
     if (const char* e = std::getenv("HP_HI_LEVELS")) q.hi_levels = std::atoll(e);  // tuning
     int threads = HP_ASYNC_MAXT;
     if (const char* e = std::getenv("HP_ASYNC_THREADS")) threads = std::atoi(e);  // tuning

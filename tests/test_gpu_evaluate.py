@@ -103,3 +103,40 @@ def test_plan_shape_rejected():
         s.tp_degree = s.dp_degree = s.nodes_used = 1
     with pytest.raises(abi.ConfigError, match="does not continue"):
         planner.engine(0).evaluate_plan_full(p, pl)
+
+
+def test_large_plans_gpipe_and_1f1b():
+    """GPipe and 1F1B at P*M >= 1e5 (the generic counter-driven evaluator and
+    the closed-form 1F1B one): batched iteration times (hp_evaluate_plans)
+    and the full evaluation with trace, against the reference."""
+    rng = random.Random(23)
+    docs = configs.config("C3", full=True)
+    L = docs["model"]["num_layers"]
+    p = abi.Problem(docs)
+    plans = []
+    for k in range(8):
+        P = rng.choice([48, 64, 80, 96])
+        M = rng.choice([1536, 2048]) if k % 2 else rng.choice([1100, 1536])
+        cuts = sorted(rng.sample(range(1, L), P - 1))
+        bounds = [0] + cuts + [L]
+        pl = abi.hp_plan()
+        pl.schedule = k % 2  # gpipe, 1f1b alternating
+        pl.micro_batches_per_dp_replica = M
+        pl.micro_batch_size = 1
+        pl.n_stages = P
+        for i in range(P):
+            s = pl.stages[i]
+            s.layer_begin, s.layer_end = bounds[i], bounds[i + 1]
+            s.group = 0 if i < P // 5 else 1
+            s.tp_degree = 8
+            s.dp_degree = 1
+            s.nodes_used = 1
+        assert P * M >= 1e5
+        plans.append(pl)
+    times = planner.engine(0).evaluate_plans(p, plans)
+    for k, pl in enumerate(plans):
+        doc = p.plan_to_doc(pl)
+        want = ref.evaluate(docs, doc)["eval"]["iteration_bits"]
+        assert bits(times[k]) == want, k
+        if k < 4:
+            check(docs, doc, f"large {k}")
