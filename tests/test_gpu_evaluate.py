@@ -115,8 +115,8 @@ def test_large_plans_gpipe_and_1f1b():
     p = abi.Problem(docs)
     plans = []
     for k in range(8):
-        P = rng.choice([48, 64, 80, 96])
-        M = rng.choice([1536, 2048]) if k % 2 else rng.choice([1100, 1536])
+        P = rng.choice([64, 80, 96])
+        M = rng.choice([1600, 2048])
         cuts = sorted(rng.sample(range(1, L), P - 1))
         bounds = [0] + cuts + [L]
         pl = abi.hp_plan()

@@ -152,3 +152,13 @@ def test_c4_c5_against_reference(engine):
                 h.update(f"{e.candidate}\t{struct.pack('>d', e.time_s).hex()}\t{e.prune_reason}\n".encode())
             assert len(out.log) == case["log"]["n"], case["name"]
             assert h.hexdigest() == case["log"]["sha256"], case["name"]
+
+
+def test_gpipe_search_at_scale(engine):
+    """GPipe search at P*M up to 98,304 (C3, pp 64, micro-batch 1, memory
+    unbounded): the generic evaluator in the climb kernel against the
+    reference's outcome (tests/golden/gen_gpipe_scale.py)."""
+    from conftest import load_golden
+    case = load_golden("gpipe_scale.json")
+    assert case["status"] == 0 and case["candidates_simulated"] > 50000
+    check_case(engine, case)
