@@ -178,10 +178,13 @@ __device__ inline void simulate_list(const Bufs& b, int li, int kind, const long
 // probe: the probe pass (planner.cpp:640-651): stop a task at its first
 // simulated seed and fold its time into *gb_bits (atomic min of the bit
 // patterns of non-negative doubles); otherwise *gb_bits is the global bound.
-__global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs b, const TaskDev* tasks, const int* order, int n_tasks,
+__global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs bg, const TaskDev* tasks, const int* order, int n_tasks,
                                                         int* next_task, TaskRes* res, int* tbest_rows, DefScratch sc,
                                                         DefSeeds sd, int seeds_ready, unsigned long long* gb_bits,
-                                                        int probe, int uniform_only) {
+                                                        int probe, int uniform_only, StagedTables tt) {
+  extern __shared__ __align__(128) unsigned char smem_tables[];
+  __shared__ __align__(8) unsigned long long tables_bar;
+  const Bufs b = stage_tables(bg, tt, smem_tables, &tables_bar);
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   long long* ids = sc.ids + (size_t)blockIdx.x * sc.CH;  // global: the evaluators read it

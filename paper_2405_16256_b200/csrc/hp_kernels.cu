@@ -131,6 +131,8 @@ struct Bufs {
   // between the current point k and path point t (prefix-sum space)
   int* memo_d;
   int nb_rows;  // kind-1 items are screened neighbours with StageLB/StageNb rows (full-mode climb)
+  int n_lg;     // LeafGroup rows / hop entries uploaded (host-side sizes for table staging)
+  int n_hop;
 };
 
 // count of bounded compositions continuing with part value v at position j
@@ -208,6 +210,62 @@ __host__ __device__ inline int eval_class(int P, int M, bool gpipe) {
 }
 
 __host__ __device__ inline int class_cpw(int cls, int P) { return 32 / class_width(cls, P); }
+
+// ------------------------------------------------------------------ table staging
+//
+// The split-independent cost tables of a search — LeafGroup rows (one per
+// distinct (dp, B, tp, nodes) tuple, ~600 for C3) and the hop table — are
+// staged once per block into shared memory with TMA bulk copies
+// (cp.async.bulk global -> shared, completion counted on an mbarrier), so
+// every stage_setup of the climb and default-mode kernels (screen rows,
+// seeds, gates, neighbour durations) reads them a few cycles away instead
+// of through L1/L2. `stage_bytes` is 0 when they do not fit (the kernels
+// then read global memory).
+struct StagedTables {
+  unsigned lg_bytes;   // LeafGroup rows, padded to 16 bytes
+  unsigned hop_bytes;  // hop table, padded to 16 bytes
+};
+
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :
+               : "r"(dst), "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// Whole block. Returns b with lg / hop pointing at the shared copies.
+__device__ inline Bufs stage_tables(const Bufs& b, const StagedTables& t, unsigned char* smem,
+                                    unsigned long long* bar) {
+  if (t.lg_bytes == 0) return b;
+  const unsigned sbar = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  const unsigned sdst = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" : : "r"(sbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" : : : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :
+                 : "r"(sbar), "r"(t.lg_bytes + t.hop_bytes)
+                 : "memory");
+    constexpr unsigned kChunk = 32768;
+    for (unsigned off = 0; off < t.lg_bytes; off += kChunk)
+      bulk_g2s(sdst + off, reinterpret_cast<const unsigned char*>(b.lg) + off, min(kChunk, t.lg_bytes - off),
+               sbar);
+    bulk_g2s(sdst + t.lg_bytes, b.hop, t.hop_bytes, sbar);
+  }
+  __syncthreads();
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+      "@!p bra WAIT_%=;\n\t}"
+      :
+      : "r"(sbar)
+      : "memory");
+  Bufs s = b;
+  s.lg = reinterpret_cast<const LeafGroup*>(smem);
+  s.hop = reinterpret_cast<const double*>(smem + t.lg_bytes);
+  return s;
+}
 
 // ------------------------------------------------------------------ seeds
 
@@ -1588,7 +1646,10 @@ __device__ __noinline__ void eval_item_call(const Bufs& b, const Work& w, int la
   eval_item<K, FAST>(b, w, lane);
 }
 
-__global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs b, AsyncQ q) {
+__global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs bg, AsyncQ q, StagedTables tt) {
+  extern __shared__ __align__(128) unsigned char smem_tables[];
+  __shared__ __align__(8) unsigned long long tables_bar;
+  const Bufs b = stage_tables(bg, tt, smem_tables, &tables_bar);
   const int lane = threadIdx.x & 31;
   long long tk[kRings] = {-1, -1, -1};
   if (q.crit_sms > 0 && (int)blockIdx.x < q.crit_sms && (threadIdx.x >> 5) >= 4) return;
@@ -2285,6 +2346,18 @@ static hph::Status consts_to_device(Arena& a, const hph::Problem& p, Consts& c) 
   return s;
 }
 
+// Shared-memory staging of the cost tables for a kernel that can give them
+// `limit` bytes of dynamic shared memory (0 = read them from global).
+static hpk::StagedTables staged(const hpk::Bufs& b, size_t limit) {
+  hpk::StagedTables t{0, 0};
+  const size_t lg = (size_t)b.n_lg * sizeof(LeafGroup), hop = (size_t)b.n_hop * sizeof(double);
+  if (b.n_lg > 0 && lg % 16 == 0 && hop % 16 == 0 && hop > 0 && lg + hop <= limit) {
+    t.lg_bytes = static_cast<unsigned>(lg);
+    t.hop_bytes = static_cast<unsigned>(hop);
+  }
+  return t;
+}
+
 static size_t split_total_of(const std::vector<Leaf>& leaves) {
   size_t n = 0;
   for (const Leaf& lf : leaves) n += lf.P;
@@ -2382,6 +2455,9 @@ static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vect
   uint8_t* d_layouts;
   double* d_hop;
   int *d_hist_off, *d_nb_off;
+  // padded to whole 16-byte units for the TMA bulk copy into shared memory
+  while ((lgs.size() * sizeof(LeafGroup)) % 16) lgs.push_back(LeafGroup{});
+  while ((hop.size() * sizeof(double)) % 16) hop.push_back(0.0);
   if (!(s = upload(a, "leaves", leaves, &d_leaves)).ok()) return s;
   if (!(s = upload(a, "lg", lgs, &d_lg)).ok()) return s;
   if (!(s = upload(a, "layouts", p.layouts, &d_layouts)).ok()) return s;
@@ -2392,6 +2468,8 @@ static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vect
   b.lg = d_lg;
   b.layouts = d_layouts;
   b.hop = d_hop;
+  b.n_lg = static_cast<int>(lgs.size());
+  b.n_hop = static_cast<int>(hop.size());
   b.hist_off = d_hist_off;
   b.nb_off = d_nb_off;
   if (!(s = scratch(a, "uni", split_total, &b.uni)).ok()) return s;
@@ -2648,7 +2726,11 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     hpk::Bufs bh = b;
     bh.nb_rows = b.log.vals == nullptr ? 1 : 0;  // the screen runs unless the log is recorded
     hpk::k_async_seed<<<(n * 32 + T - 1) / T, T, 0, st>>>(bh, q, d_climb, n);
-    hpk::k_hill_async<<<grid, threads, 0, st>>>(bh, q);
+    // one block per SM: up to 160 KB of tables in shared memory
+    const hpk::StagedTables tt = staged(bh, std::getenv("HP_NO_STAGE") ? 0 : 160 * 1024);  // (knob: A/B)
+    const size_t dsm = tt.lg_bytes + tt.hop_bytes;
+    if (dsm > 48 * 1024) CK(cudaFuncSetAttribute(hpk::k_hill_async, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    hpk::k_hill_async<<<grid, threads, dsm, st>>>(bh, q, tt);
     if (h1) CK(cudaEventRecord(h1, st));
     out.launches += 2;
     out.eval_launches++;
@@ -3187,8 +3269,11 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   int* d_order;
   if (!(s = upload(a, "d_order", order, &d_order)).ok()) return s;
   const int threads = hpk::DEF_THREADS;
+  const hpk::StagedTables tt = staged(b, std::getenv("HP_NO_STAGE") ? 0 : 80 * 1024);  // (knob: A/B)
+  const size_t dsm = tt.lg_bytes + tt.hop_bytes;
+  if (dsm > 48 * 1024) CK(cudaFuncSetAttribute(hpk::k_default, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hpk::k_default, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hpk::k_default, threads, dsm);
   const int blocks = std::min(nT, a.sm_count * std::max(1, per_sm));
   hpk::DefScratch sc;
   sc.CH = hpk::DEF_CH;
@@ -3229,8 +3314,8 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   }
   if (!have_bound) {
     CK(cudaMemsetAsync(d_next, 0, sizeof(int), st));
-    hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, d_order, nT, d_next, d_res, d_tbest, sc, sd, 0, d_gb,
-                                               1, p.uniform_only ? 1 : 0);
+    hpk::k_default<<<blocks, threads, dsm, st>>>(b, d_tasks, d_order, nT, d_next, d_res, d_tbest, sc, sd, 0, d_gb,
+                                                 1, p.uniform_only ? 1 : 0, tt);
     out.launches++;
     out.eval_launches++;
     if (probe_only) {
@@ -3254,8 +3339,8 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
     cudaEventRecord(e0, st);
   }
   // the probe pass computed every leaf's seeds (and simulated some)
-  hpk::k_default<<<blocks, threads, 0, st>>>(b, d_tasks, d_order, nT, d_next, d_res, d_tbest, sc, sd,
-                                             have_bound ? 0 : 1, d_gb, 0, p.uniform_only ? 1 : 0);
+  hpk::k_default<<<blocks, threads, dsm, st>>>(b, d_tasks, d_order, nT, d_next, d_res, d_tbest, sc, sd,
+                                               have_bound ? 0 : 1, d_gb, 0, p.uniform_only ? 1 : 0, tt);
   if (a.time_evals) cudaEventRecord(e1, st);
   out.launches++;
   out.eval_launches++;

@@ -1,0 +1,7 @@
+#!/bin/bash
+# N-GPU bench (torchrun, one rank per GPU), as the driver runs it
+cd "$GRAFT_REPO_ROOT"
+mkdir -p gpurun_out
+N=$(nvidia-smi -L | wc -l)
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus $N --steps 5 --warmup 3 > gpurun_out/scale_n$N.json 2> gpurun_out/scale_n$N.err
+echo "rc=$?" >> gpurun_out/scale_n$N.err
