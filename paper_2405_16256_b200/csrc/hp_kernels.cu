@@ -2729,7 +2729,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     // one block per SM: up to 160 KB of tables in shared memory
     const hpk::StagedTables tt = staged(bh, std::getenv("HP_NO_STAGE") ? 0 : 160 * 1024);  // (knob: A/B)
     const size_t dsm = tt.lg_bytes + tt.hop_bytes;
-    if (dsm > 48 * 1024) CK(cudaFuncSetAttribute(hpk::k_hill_async, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    CK(cudaFuncSetAttribute(hpk::k_hill_async, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
     hpk::k_hill_async<<<grid, threads, dsm, st>>>(bh, q, tt);
     if (h1) CK(cudaEventRecord(h1, st));
     out.launches += 2;
@@ -3271,9 +3271,14 @@ hph::Status search_default(Arena& a, const hph::Problem& p, const std::vector<in
   const int threads = hpk::DEF_THREADS;
   const hpk::StagedTables tt = staged(b, std::getenv("HP_NO_STAGE") ? 0 : 80 * 1024);  // (knob: A/B)
   const size_t dsm = tt.lg_bytes + tt.hop_bytes;
-  if (dsm > 48 * 1024) CK(cudaFuncSetAttribute(hpk::k_default, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  // (always set: the default cap on dynamic shared memory is 48 KB minus the
+  // kernel's static shared memory)
+  CK(cudaFuncSetAttribute(hpk::k_default, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hpk::k_default, threads, dsm);
+  if (std::getenv("HP_DEBUG_LAUNCH"))
+    std::fprintf(stderr, "k_default: tasks %d leaves %zu rows %d hop %d dsm %zu per_sm %d\n", nT, my_leaves.size(),
+                 b.n_lg, b.n_hop, dsm, per_sm);
   const int blocks = std::min(nT, a.sm_count * std::max(1, per_sm));
   hpk::DefScratch sc;
   sc.CH = hpk::DEF_CH;

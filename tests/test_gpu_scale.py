@@ -104,3 +104,24 @@ def test_climb_scheduling_does_not_change_results(engine, knobs):
         assert (x.candidates_simulated, x.candidates_pruned) == (ref.candidates_simulated, ref.candidates_pruned)
         assert x.best_time_s == ref.best_time_s
         assert abi.encode_plan(p.group_names, x.best_plan) == abi.encode_plan(p.group_names, ref.best_plan)
+
+
+def test_default_mode_shards_in_fresh_process():
+    """A sharded default-mode search as each rank of a multi-GPU run does it,
+    in a fresh process (kernel attributes set by no earlier search): probe,
+    search with a bound, no error, and every shard's counts add up."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2405_16256_b200 import abi, configs, planner\n"
+            "eng = planner.engine(0)\n"
+            "p = abi.Problem(configs.config('C3', full=False))\n"
+            "b = min(eng.probe_shard(p, s, 4) for s in range(4))\n"
+            "rs = [eng.search_shard(p, s, 4, b) for s in range(4)]\n"
+            "red = planner.reduce_results(p, rs)\n"
+            "print(red.candidates_simulated, red.candidates_pruned, repr(red.best_time_s))\n" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    sim, pr, t = out.stdout.split()
+    assert (int(sim), int(pr), float(t)) == (1866, 216837, C3_TIME)
