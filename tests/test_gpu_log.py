@@ -99,6 +99,63 @@ def test_c3_default_log_matches_reference(engine):
     assert digest(got) == want["sha256"]
 
 
+def test_c3_full_log_matches_reference_per_pp(engine):
+    """C3 full sweep with the log (10,513,178 entries): for every pipeline
+    degree, the entry count, the simulated / pruned split and the SHA-256 of
+    that pp's slice of the log equal the compiled reference's, run one pp job
+    at a time (tests/golden/gen_c3_full_ref.py; ~36 CPU-hours)."""
+    import ctypes as C
+    import json as J
+    import numpy as np
+    from paper_2405_16256_b200 import configs
+    want = load_golden("c3_full_ref.json")["per_pp"]
+    p = abi.Problem(configs.config("C3", full=True))
+    res = engine.search_shard(p, flags=abi.HP_FLAG_LOG)
+    n, nb = C.c_uint64(), C.c_uint64()
+    assert engine._lib.hp_search_log(engine._ctx, None, 0, None, 0, C.byref(n), C.byref(nb)) == abi.HP_OK
+    assert n.value == res.candidates_simulated + res.candidates_pruned == 10513178
+    ents = (abi.hp_log_entry * n.value)()
+    text = C.create_string_buffer(nb.value)
+    assert engine._lib.hp_search_log(engine._ctx, ents, n.value, text, nb.value, C.byref(n), C.byref(nb)) == abi.HP_OK
+    e = np.frombuffer(ents, dtype=np.dtype([("c", "<u8"), ("r", "<u8"), ("t", "<f8"), ("task", "<i4"),
+                                            ("leaf", "<i4")]))
+    raw = text.raw
+    cs, rs, tasks = e["c"].tolist(), e["r"].tolist(), e["task"].tolist()
+    bl = e["t"].view("<u8").tolist()
+    got = {}
+    cur_task, pp, h, sim, pru = None, None, None, 0, 0
+
+    def flush():
+        if pp is not None:
+            d = got.setdefault(pp, [hashlib.sha256(), 0, 0])
+            d[0] = h
+            d[1] += sim
+            d[2] += pru
+
+    for k in range(n.value):
+        c0 = cs[k]
+        cand = raw[c0:raw.index(b"\0", c0)]
+        if tasks[k] != cur_task:
+            cur_task = tasks[k]
+            npp = J.loads(cand)["pp"]
+            if npp != pp:
+                flush()
+                pp, h, sim, pru = npp, hashlib.sha256(), 0, 0
+        r0 = rs[k]
+        reason = raw[r0:raw.index(b"\0", r0)]
+        h.update(cand + b"\t" + b"%016x" % bl[k] + b"\t" + reason + b"\n")
+        if reason:
+            pru += 1
+        else:
+            sim += 1
+    flush()
+    assert sorted(got) == sorted(int(k) for k in want)
+    for pp, (hh, s_, p_) in got.items():
+        w = want[str(pp)]
+        assert (s_, p_) == (w["simulated"], w["pruned"]), pp
+        assert hh.hexdigest() == w["sha256"], pp
+
+
 def test_c3_full_log_is_complete(engine):
     """C3 full sweep with the log (10.5 M entries; the reference needs ~8 CPU-
     hours for it, so no digest): the replay consumes every GPU time and its

@@ -40,11 +40,25 @@ def test_c3_full_sweep(engine):
     assert a.best_time_s == b.best_time_s == C3_TIME
     assert abi.encode_plan(p.group_names, a.best_plan) == C3_PLAN
     assert (a.candidates_simulated, a.candidates_pruned) == (b.candidates_simulated, b.candidates_pruned)
-    pinned = os.path.join(GOLDEN, "c3_full_counts.json")
-    if os.path.exists(pinned):
-        want = json.load(open(pinned))
-        assert (a.candidates_simulated, a.candidates_pruned) == (want["candidates_simulated"],
-                                                                 want["candidates_pruned"])
+    # pinned by the compiled reference itself, one search per pp job
+    # (tests/golden/gen_c3_full_ref.py)
+    want = json.load(open(os.path.join(GOLDEN, "c3_full_ref.json")))
+    assert (a.candidates_simulated, a.candidates_pruned) == (want["candidates_simulated"],
+                                                             want["candidates_pruned"])
+    assert a.best_time_s == want["best_iteration_time_s"]
+    assert abi.encode_plan(p.group_names, a.best_plan) == abi.encode_plan(p.group_names,
+                                                                          p.plan_from_doc(want["best_plan"]))
+
+
+@pytest.mark.parametrize("pps", [[12], [24], [64], [88], [89, 90], [91, 92], [93, 94], [95, 96]])
+def test_c3_full_sweep_per_pp_counts(engine, pps):
+    """Per-pp slices of the sweep — the long-climb regime (pp 88-96) in
+    particular — against the reference's per-pp counts."""
+    want = json.load(open(os.path.join(GOLDEN, "c3_full_ref.json")))["per_pp"]
+    p = abi.Problem(configs.with_pp(configs.config("C3", full=True), pps))
+    r = engine.search_shard(p)
+    assert r.candidates_simulated == sum(want[str(x)]["simulated"] for x in pps)
+    assert r.candidates_pruned == sum(want[str(x)]["pruned"] for x in pps)
 
 
 @pytest.mark.parametrize("count", [2, 3, 8])
@@ -100,8 +114,12 @@ def test_climb_scheduling_does_not_change_results(engine, knobs):
             else:
                 os.environ[k] = v
     ref = engine.search_shard(p)
-    for x in (r, rl):
-        assert (x.candidates_simulated, x.candidates_pruned) == (ref.candidates_simulated, ref.candidates_pruned)
+    # the compiled reference's per-pp counts (tests/golden/c3_full_ref.json)
+    want = json.load(open(os.path.join(GOLDEN, "c3_full_ref.json")))["per_pp"]
+    sims = sum(want[str(x)]["simulated"] for x in (12, 88, 92, 96))
+    prs = sum(want[str(x)]["pruned"] for x in (12, 88, 92, 96))
+    for x in (r, rl, ref):
+        assert (x.candidates_simulated, x.candidates_pruned) == (sims, prs)
         assert x.best_time_s == ref.best_time_s
         assert abi.encode_plan(p.group_names, x.best_plan) == abi.encode_plan(p.group_names, ref.best_plan)
 
