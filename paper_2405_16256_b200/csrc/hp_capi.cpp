@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -148,6 +150,7 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   hph::Problem p;
   hp_status st = prepare(ctx, problem, p);
   if (st != HP_OK) return st;
+  const auto h_prep = std::chrono::steady_clock::now();
   int shard = opts ? opts->shard_index : 0;
   int nshard = opts && opts->shard_count > 0 ? opts->shard_count : 1;
   if (shard < 0 || shard >= nshard) return fail(ctx, HP_BAD_CONFIG, "bad shard index");
@@ -210,6 +213,13 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   float ms = 0;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   result->device_ms = ms;
+  if (std::getenv("HP_DEBUG_TIMING")) {  // diagnostics: host phases of this call
+    const auto h_end = std::chrono::steady_clock::now();
+    auto dms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "hp_search: prepare %.2f ms, shard %.2f ms, search+log %.2f ms (device %.2f ms)\n",
+                 dms(h0, h_prep), result->host_ms - dms(h0, h_prep), dms(h_prep, h_end) - (result->host_ms - dms(h0, h_prep)),
+                 ms);
+  }
   result->gpu_launches = out.launches;
   result->eval_launches = out.eval_launches;
   result->eval_ms = out.eval_ms;

@@ -8,6 +8,7 @@
 #include <numeric>
 #include <set>
 #include <sstream>
+#include <thread>
 
 namespace hph {
 
@@ -218,34 +219,19 @@ void compositions(Problem& p, int pp, int g, int remaining, std::vector<int>& cu
 
 }  // namespace
 
-void enumerate(Problem& p) {
-  p.tasks.clear();
-  p.leaves.clear();
-  p.layouts.clear();
+namespace {
+
+// run_task's leaves of tasks [t0, t1) into out / tp (task-local tp_base and
+// leaf_begin / leaf_end offsets, rebased by the caller).
+void enumerate_leaves(Problem& p, int t0, int t1, const std::vector<long long>& dps, std::vector<LeafHost>& out,
+                      std::vector<int32_t>& tp_out) {
   const int G = static_cast<int>(p.groups.size());
   const int L = p.model.num_layers;
-  for (int pp : p.pps) {
-    if (pp < 1 || pp > L) continue;
-    std::vector<int> cur;
-    compositions(p, pp, 0, pp, cur);
-  }
-  // dp values some micro-batch candidate divides the global batch with
-  // (planner.cpp:355-357), descending; a task walks them from its dp_max
-  long long dp_cap = 1;
-  for (int g = 0; g < G; ++g)
-    dp_cap = std::max(dp_cap, static_cast<long long>(p.groups[g].node_count) * p.groups[g].devices_per_node);
-  std::vector<long long> dps;
-  for (long long dp = dp_cap; dp >= 1; --dp)
-    for (int64_t B : p.mbs)
-      if (p.train.global_batch_size % (dp * B) == 0) {
-        dps.push_back(dp);
-        break;
-      }
-  for (int ti = 0; ti < static_cast<int>(p.tasks.size()); ++ti) {
+  std::vector<std::vector<int>> tpo(G), okt(G);
+  std::vector<size_t> idx(G);
+  for (int ti = t0; ti < t1; ++ti) {
     Task& t = p.tasks[ti];
-    t.layout_off = static_cast<int>(p.layouts.size());
-    for (int g : t.layout) p.layouts.push_back(static_cast<uint8_t>(g));
-    t.leaf_begin = t.leaf_end = static_cast<int>(p.leaves.size());
+    t.leaf_begin = t.leaf_end = static_cast<int>(out.size());
     for (int i = 0; i + 1 < t.pp; ++i) {
       int a = t.layout[i], b = t.layout[i + 1];
       if (a != b && p.pair[a][b] < 0) {
@@ -260,19 +246,18 @@ void enumerate(Problem& p) {
       long long nps = p.groups[g].node_count / t.spg[g];
       dp_max = std::min(dp_max, nps * p.groups[g].devices_per_node);
     }
-    std::vector<std::vector<int>> tpo(G, std::vector<int>{1});
-    for (int g = 0; g < G; ++g)
+    for (int g = 0; g < G; ++g) {
+      tpo[g].assign(1, 1);
       if (t.spg[g] > 0) {
         tpo[g].clear();
         for (int d = 1; d <= p.groups[g].devices_per_node; ++d)
           if (p.groups[g].devices_per_node % d == 0) tpo[g].push_back(d);
       }
+    }
     const long long nsplit = hpc::contiguous_split_count(L, t.pp);
     // The allotment test (planner.cpp:366-379) is per group, so the leaves
     // of a (dp, B) are the product of each group's passing tp values, in the
     // odometer order (group 0 fastest) restricted to them.
-    std::vector<std::vector<int>> okt(G);
-    std::vector<size_t> idx(G);
     for (long long dp : dps) {
       if (dp > dp_max) continue;
       bool empty = false;
@@ -303,24 +288,87 @@ void enumerate(Problem& p) {
           lf.B = B;
           lf.B_idx = bi;
           lf.M = p.train.global_batch_size / (dp * B);
-          for (int g = 0; g < HP_MAX_GROUPS; ++g) {
-            lf.tp[g] = g < G ? okt[g][idx[g]] : 1;
-            lf.nodes[g] = 0;
-          }
-          for (int g = 0; g < G; ++g)
-            if (t.spg[g] > 0) lf.nodes[g] = static_cast<int>(dp * lf.tp[g] / p.groups[g].devices_per_node);
+          lf.tp_base = static_cast<int>(tp_out.size());
+          for (int g = 0; g < G; ++g) tp_out.push_back(okt[g][idx[g]]);
           lf.n_splits = nsplit;
           lf.exhaustive = !p.uniform_only && nsplit <= p.limit;
           double pm = static_cast<double>(t.pp) * static_cast<double>(lf.M);
           lf.cost = lf.exhaustive ? pm * static_cast<double>(nsplit) : pm * (2.0 + 12.0 * 2.0 * (t.pp - 1));
-          p.leaves.push_back(lf);
+          out.push_back(lf);
           int g = 0;
           while (g < G && ++idx[g] == okt[g].size()) idx[g++] = 0;
           if (g == G) break;
         }
       }
     }
-    t.leaf_end = static_cast<int>(p.leaves.size());
+    t.leaf_end = static_cast<int>(out.size());
+  }
+}
+
+}  // namespace
+
+void enumerate(Problem& p) {
+  p.tasks.clear();
+  p.leaves.clear();
+  p.leaf_tp.clear();
+  p.layouts.clear();
+  const int G = static_cast<int>(p.groups.size());
+  const int L = p.model.num_layers;
+  for (int pp : p.pps) {
+    if (pp < 1 || pp > L) continue;
+    std::vector<int> cur;
+    compositions(p, pp, 0, pp, cur);
+  }
+  for (Task& t : p.tasks) {
+    t.layout_off = static_cast<int>(p.layouts.size());
+    for (int g : t.layout) p.layouts.push_back(static_cast<uint8_t>(g));
+  }
+  // dp values some micro-batch candidate divides the global batch with
+  // (planner.cpp:355-357), descending; a task walks them from its dp_max
+  long long dp_cap = 1;
+  for (int g = 0; g < G; ++g)
+    dp_cap = std::max(dp_cap, static_cast<long long>(p.groups[g].node_count) * p.groups[g].devices_per_node);
+  std::vector<long long> dps;
+  for (long long dp = dp_cap; dp >= 1; --dp)
+    for (int64_t B : p.mbs)
+      if (p.train.global_batch_size % (dp * B) == 0) {
+        dps.push_back(dp);
+        break;
+      }
+  // Tasks are independent here: contiguous task ranges on host threads,
+  // concatenated in task order (the reference's leaf order).
+  const int T = static_cast<int>(p.tasks.size());
+  const int nth = std::max(1, std::min({T / 256, 8, static_cast<int>(std::thread::hardware_concurrency())}));
+  std::vector<std::vector<LeafHost>> part(nth);
+  std::vector<std::vector<int32_t>> part_tp(nth);
+  std::vector<std::thread> th;
+  for (int k = 0; k < nth; ++k) {
+    const int t0 = static_cast<int>(static_cast<long long>(T) * k / nth);
+    const int t1 = static_cast<int>(static_cast<long long>(T) * (k + 1) / nth);
+    if (nth == 1) enumerate_leaves(p, t0, t1, dps, part[k], part_tp[k]);
+    else th.emplace_back(enumerate_leaves, std::ref(p), t0, t1, std::cref(dps), std::ref(part[k]), std::ref(part_tp[k]));
+  }
+  for (auto& x : th) x.join();
+  size_t nl = 0, ntp = 0;
+  for (int k = 0; k < nth; ++k) {
+    nl += part[k].size();
+    ntp += part_tp[k].size();
+  }
+  p.leaves.reserve(nl);
+  p.leaf_tp.reserve(ntp);
+  for (int k = 0; k < nth; ++k) {
+    const int t0 = static_cast<int>(static_cast<long long>(T) * k / nth);
+    const int t1 = static_cast<int>(static_cast<long long>(T) * (k + 1) / nth);
+    const int lo = static_cast<int>(p.leaves.size()), to = static_cast<int>(p.leaf_tp.size());
+    for (int ti = t0; ti < t1; ++ti) {
+      p.tasks[ti].leaf_begin += lo;
+      p.tasks[ti].leaf_end += lo;
+    }
+    for (LeafHost& lf : part[k]) {
+      lf.tp_base += to;
+      p.leaves.push_back(lf);
+    }
+    p.leaf_tp.insert(p.leaf_tp.end(), part_tp[k].begin(), part_tp[k].end());
   }
 }
 
@@ -434,7 +482,7 @@ hpc::Leaf device_leaf(const Problem& p, int li) {
 void leaf_rows(const Problem& p, int li, hpc::LeafGroup* rows) {
   const LeafHost& h = p.leaves[li];
   for (int g = 0; g < static_cast<int>(p.groups.size()); ++g)
-    rows[g] = leaf_group(p, g, h.tp[g], h.B, h.dp, h.nodes[g]);
+    rows[g] = leaf_group(p, g, leaf_tp(p, h, g), h.B, h.dp, leaf_nodes(p, h, g));
 }
 
 std::vector<double> hop_table(const Problem& p) {
@@ -513,7 +561,7 @@ void make_plan(const Problem& p, const LeafHost& lf, const int* split, hp_plan& 
     s.layer_end = begin + split[i];
     begin += split[i];
     s.group = g;
-    s.tp_degree = lf.tp[g];
+    s.tp_degree = leaf_tp(p, lf, g);
     s.dp_degree = lf.dp;
     s.nodes_used = static_cast<int>(static_cast<long long>(lf.dp) * s.tp_degree /
                                     p.groups[g].devices_per_node);

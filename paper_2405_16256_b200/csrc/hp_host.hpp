@@ -36,8 +36,7 @@ struct LeafHost {
   int64_t B;
   int B_idx;
   int64_t M;
-  int tp[HP_MAX_GROUPS];
-  int nodes[HP_MAX_GROUPS];
+  int tp_base;          // this leaf's tp per group: Problem::leaf_tp[tp_base + g]
   bool exhaustive;
   long long n_splits;   // C(L-1, pp-1), saturating
   double cost;          // work estimate for sharding
@@ -65,6 +64,7 @@ struct Problem {
   // enumeration
   std::vector<Task> tasks;
   std::vector<LeafHost> leaves;
+  std::vector<int32_t> leaf_tp;  // G per leaf (1 for groups the task leaves out)
   std::vector<uint8_t> layouts;  // concatenated task layouts
   int total_nodes = 0;
 };
@@ -76,6 +76,14 @@ Status load_problem(const hp_problem* in, Problem& p);
 // build_tasks (planner.cpp:238-304) and the leaf enumeration of run_task
 // (planner.cpp:312-393), in reference order.
 void enumerate(Problem& p);
+
+// tp and nodes_used of group g in leaf h (planner.cpp:366-379: nodes =
+// dp * tp / devices_per_node where the task has stages of g, else 0).
+inline int leaf_tp(const Problem& p, const LeafHost& h, int g) { return p.leaf_tp[h.tp_base + g]; }
+inline int leaf_nodes(const Problem& p, const LeafHost& h, int g) {
+  if (p.tasks[h.task].spg[g] == 0) return 0;
+  return static_cast<int>(static_cast<long long>(h.dp) * leaf_tp(p, h, g) / p.groups[g].devices_per_node);
+}
 
 // Exact-order cost terms.
 double hop_time(const Problem& p, int link, int64_t B);            // cost_model.cpp:43-61

@@ -2428,8 +2428,8 @@ static hph::Status setup_tables(Arena& a, const hph::Problem& p, const std::vect
     key[1] = h.B_idx;
     key[2] = h.B;
     for (int g = 0; g < G; ++g) {
-      key[3 + 2 * g] = h.tp[g];
-      key[4 + 2 * g] = h.nodes[g];
+      key[3 + 2 * g] = hph::leaf_tp(p, h, g);
+      key[4 + 2 * g] = hph::leaf_nodes(p, h, g);
     }
     auto it = row_of.find(key);
     if (it == row_of.end()) {

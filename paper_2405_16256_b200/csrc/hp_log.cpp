@@ -69,7 +69,7 @@ LeafDesc leaf_desc(const hph::Problem& p, const hph::LeafHost& h) {
              ",\"pp\":" + std::to_string(t.pp) + ",\"split\":[";
   std::map<std::string, int> tp;  // std::map: nlohmann's object key order
   for (size_t g = 0; g < p.groups.size(); ++g)
-    if (t.spg[g] > 0) tp.emplace(p.groups[g].name, h.tp[g]);
+    if (t.spg[g] > 0) tp.emplace(p.groups[g].name, hph::leaf_tp(p, h, static_cast<int>(g)));
   d.suffix = "],\"tp\":{";
   bool first = true;
   for (const auto& kv : tp) {

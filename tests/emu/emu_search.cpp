@@ -72,7 +72,8 @@ extern "C" int emu_search_shard(const hp_problem* in, int shard, int count, hp_r
     LeafDev L;
     L.lf = Leaf{h.task, t.pp, (int)h.M, h.dp, h.B, h.B_idx, t.layout_off, 0, 0,
                 p.uniform_only ? 2 : (h.exhaustive ? 1 : 0), 0};
-    for (int g = 0; g < G; ++g) L.lg.push_back(hph::leaf_group(p, g, h.tp[g], h.B, h.dp, h.nodes[g]));
+    for (int g = 0; g < G; ++g)
+      L.lg.push_back(hph::leaf_group(p, g, hph::leaf_tp(p, h, g), h.B, h.dp, hph::leaf_nodes(p, h, g)));
     L.slots = &p.layouts[t.layout_off];
     L.hop = &hop[h.B_idx * p.links.size()];
     const int P = t.pp;
