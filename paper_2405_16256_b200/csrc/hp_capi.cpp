@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <string>
 
 #include "../../include/hetplan_b200.h"
@@ -21,6 +22,11 @@ struct hp_ctx {
   std::string err;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   hpl::Log log;  // of the last hp_search with HP_FLAG_LOG
+  // The enumerated problem of the last hp_probe, handed to the next
+  // hp_search of the same problem (a sharded default-mode search calls both
+  // per search); one-shot, so every search still enumerates once.
+  std::unique_ptr<hph::Problem> probed;
+  std::string probed_key;
 };
 
 namespace {
@@ -35,6 +41,36 @@ hp_status fail(hp_ctx* ctx, const hph::Status& s) {
 
 hp_status fail(hp_ctx* ctx, hp_status code, const std::string& m) {
   return fail(ctx, hph::Status{code, m});
+}
+
+// The inputs of a problem, byte for byte (struct fields, arrays and names).
+std::string problem_key(const hp_problem* in) {
+  std::string k;
+  auto put = [&k](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+  put(&in->model, sizeof in->model);
+  put(&in->train, sizeof in->train);
+  for (int g = 0; g < in->cluster.n_groups; ++g) {
+    hp_group x = in->cluster.groups[g];
+    const char* nm = x.name ? x.name : "";
+    x.name = nullptr;
+    put(&x, sizeof x);
+    k.append(nm);
+    k.push_back('\0');
+  }
+  for (int l = 0; l < in->cluster.n_links; ++l) {
+    hp_link x = in->cluster.links[l];
+    x.group_a_name = x.group_b_name = nullptr;
+    put(&x, sizeof x);
+  }
+  hp_planner pl = in->planner;
+  pl.pipeline_degrees = nullptr;
+  pl.micro_batch_candidates = nullptr;
+  put(&pl, sizeof pl);
+  if (in->planner.n_pipeline_degrees > 0)
+    put(in->planner.pipeline_degrees, sizeof(int32_t) * in->planner.n_pipeline_degrees);
+  if (in->planner.n_micro_batch_candidates > 0)
+    put(in->planner.micro_batch_candidates, sizeof(int64_t) * in->planner.n_micro_batch_candidates);
+  return k;
 }
 
 hp_status prepare(hp_ctx* ctx, const hp_problem* problem, hph::Problem& p) {
@@ -126,7 +162,9 @@ hp_status hp_probe(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts*
   if (!ctx || !bound) return HP_INTERNAL;
   cudaSetDevice(ctx->arena.device);
   *bound = std::numeric_limits<double>::infinity();
-  hph::Problem p;
+  ctx->probed.reset();
+  auto pp = std::make_unique<hph::Problem>();
+  hph::Problem& p = *pp;
   hp_status st = prepare(ctx, problem, p);
   if (st != HP_OK) return st;
   int shard = opts ? opts->shard_index : 0;
@@ -138,6 +176,8 @@ hp_status hp_probe(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts*
                                       true, out);
   if (!s.ok()) return fail(ctx, s);
   *bound = out.global_bound;
+  ctx->probed_key = problem_key(problem);
+  ctx->probed = std::move(pp);
   return HP_OK;
 }
 
@@ -147,9 +187,15 @@ hp_status hp_search(hp_ctx* ctx, const hp_problem* problem, const hp_search_opts
   cudaSetDevice(ctx->arena.device);
   std::memset(result, 0, sizeof(*result));
   auto h0 = std::chrono::steady_clock::now();
-  hph::Problem p;
-  hp_status st = prepare(ctx, problem, p);
-  if (st != HP_OK) return st;
+  std::unique_ptr<hph::Problem> probed = std::move(ctx->probed);
+  if (probed && ctx->probed_key != problem_key(problem)) probed.reset();
+  std::unique_ptr<hph::Problem> own;
+  if (!probed) {
+    own = std::make_unique<hph::Problem>();
+    hp_status st = prepare(ctx, problem, *own);
+    if (st != HP_OK) return st;
+  }
+  hph::Problem& p = probed ? *probed : *own;
   const auto h_prep = std::chrono::steady_clock::now();
   int shard = opts ? opts->shard_index : 0;
   int nshard = opts && opts->shard_count > 0 ? opts->shard_count : 1;
