@@ -358,7 +358,46 @@ __device__ __forceinline__ void eval_item_generic(const Bufs& b, const Work& w, 
     StageState st[K];
 #pragma unroll
     for (int r = 0; r < K; ++r) stage_init(st[r]);
-    if (__any_sync(0xffffffffu, run)) {
+    if (gpipe && __any_sync(0xffffffffu, run)) {
+      // GPipe in closed form: the unit-time ASAP level of F(i,m) is i+m and
+      // that of B(i,j) is 2P-2-i+M+j (F(i,m) needs F(i-1,m)'s send, one
+      // level earlier; B(P-1,0) follows the last forward of the last stage;
+      // B(i,j) needs B(i+1,j)'s send). So all forwards run in levels
+      // [0, M+P-2] and all backwards in [M+P-1, 2M+2P-3]: a forward
+      // wavefront (stage i active in [i, i+M-1]) and a backward one (stage i
+      // active in [P-1-i, P-2-i+M] of the second phase), each stage reading
+      // its neighbour's channel from the previous level (single slot, as in
+      // the counter-driven path below) — no counters, no readiness tests.
+      const int LV = M + P - 1;
+      for (int t = 0; t < LV; ++t) {
+        const double lchf = __shfl_up_sync(0xffffffffu, st[K - 1].chf, 1);
+#pragma unroll
+        for (int r = K - 1; r >= 0; --r) {  // descending: chf[r-1] is still the previous level's
+          const int i = sl * K + r;
+          const double recv = i == 0 ? 0.0 : (r == 0 ? lchf : st[r > 0 ? r - 1 : 0].chf);
+          const double nfr = dmax(st[r].free_t, recv) + d[r].f;   // sim.cpp:106-121
+          const double nch = dmax(nfr, st[r].chf) + d[r].sf;      // sim.cpp:125-134
+          if (run && i < P && t >= i && t <= i + M - 1) {
+            st[r].free_t = nfr;
+            if (i < P - 1) st[r].chf = nch;
+          }
+        }
+      }
+      for (int t = 0; t < LV; ++t) {
+        const double rchb = __shfl_down_sync(0xffffffffu, st[0].chb, 1);
+#pragma unroll
+        for (int r = 0; r < K; ++r) {  // ascending: chb[r+1] is still the previous level's
+          const int i = sl * K + r;
+          const double recv = i == P - 1 ? 0.0 : (r == K - 1 ? rchb : st[r < K - 1 ? r + 1 : 0].chb);
+          const double nfr = dmax(st[r].free_t, recv) + d[r].b;
+          const double nch = dmax(nfr, st[r].chb) + d[r].sb;      // sim.cpp:135-145
+          if (run && i < P && t >= P - 1 - i && t <= P - 2 - i + M) {
+            st[r].free_t = nfr;
+            if (i > 0) st[r].chb = nch;
+          }
+        }
+      }
+    } else if (__any_sync(0xffffffffu, run)) {
       for (;;) {
         bool done = true;
 #pragma unroll
