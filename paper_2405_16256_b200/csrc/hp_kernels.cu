@@ -1680,10 +1680,20 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int 
 #define HP_ASYNC_MAXT 256
 #endif
 
+#ifndef HP_EVAL_INLINE
+#define HP_EVAL_INLINE 0  // tuning: 1 inlines the evaluators into the climb kernel
+#endif
+#if HP_EVAL_INLINE
+template <int K, bool FAST>
+__device__ __forceinline__ void eval_item_call(const Bufs& b, const Work& w, int lane) {
+  eval_item<K, FAST>(b, w, lane);
+}
+#else
 template <int K, bool FAST>
 __device__ __noinline__ void eval_item_call(const Bufs& b, const Work& w, int lane) {
   eval_item<K, FAST>(b, w, lane);
 }
+#endif
 
 __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs bg, AsyncQ q, StagedTables tt) {
   extern __shared__ __align__(128) unsigned char smem_tables[];
