@@ -96,7 +96,8 @@ def test_gpipe_and_short_pipelines(engine, oracle_port):
 
 
 def test_evaluate_plans_bit_exact(engine, oracle_port):
-    """hp_evaluate_plans == evaluate_plan_unchecked(...).iteration_time_s."""
+    """hp_evaluate_plans == evaluate_plan_unchecked(...).iteration_time_s of
+    the compiled reference (and of the C restatement)."""
     rng = random.Random(5)
     docs = configs.config("C0", full=True)
     p = abi.Problem(docs)
@@ -122,8 +123,11 @@ def test_evaluate_plans_bit_exact(engine, oracle_port):
             s.nodes_used = rng.choice([1, 2])
         plans.append(pl)
     got = engine.evaluate_plans(p, plans)
+    from oracle import ref
     for pl, g in zip(plans, got):
         assert g == oracle_port.evaluate(p, pl)
+        want = ref.evaluate(docs, p.plan_to_doc(pl))["eval"]["iteration_bits"]
+        assert hexbits(g) == want
 
 
 def test_bad_config_raises_config_error(engine):
