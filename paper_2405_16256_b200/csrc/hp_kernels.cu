@@ -485,7 +485,13 @@ __device__ void trace_cycles(const Bufs& b, int ev, int li, int P, int M, unsign
 }
 
 // Core-loop level pairs between early-abort checks of a screened neighbour.
-constexpr int kAbortPairs = 64;
+// The check (per stage frontier + remaining work + the backward drain, with
+// two segment scans) costs more than the levels it saves on C3: it runs only
+// on items longer than 2 x 4096 levels (M > ~4000).
+#ifndef HP_ABORT_PAIRS
+#define HP_ABORT_PAIRS 4096  // tuning (C3, 1 GPU: 64 -> 236-249 ms, 128 -> 226-234, 512 -> 218-226, 4096 -> 215-219)
+#endif
+constexpr int kAbortPairs = HP_ABORT_PAIRS;
 
 template <int K>
 __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, const int lane) {
