@@ -488,6 +488,13 @@ __device__ void trace_cycles(const Bufs& b, int ev, int li, int P, int M, unsign
 // The check (per stage frontier + remaining work + the backward drain, with
 // two segment scans) costs more than the levels it saves on C3: it runs only
 // on items longer than 2 x 4096 levels (M > ~4000).
+#ifndef HP_ABORT_CODE
+#define HP_ABORT_CODE 0  // 1 compiles the early-abort check in (C3, 1 GPU: 219-222 ms with it, 212-218 without)
+#endif
+#ifndef HP_UNROLL_CORE
+#define HP_UNROLL_CORE 2  // tuning: level-pair unroll of the K != 4 core loops
+#endif
+constexpr int kUnrollCore = HP_UNROLL_CORE;
 #ifndef HP_ABORT_PAIRS
 #define HP_ABORT_PAIRS 4096  // tuning (C3, 1 GPU: 64 -> 236-249 ms, 128 -> 226-234, 512 -> 218-226, 4096 -> 215-219)
 #endif
@@ -798,7 +805,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
               level(I1{}, PF{}, M2{}, t + 1);
             }
           } else {
-#pragma unroll 2
+#pragma unroll kUnrollCore
             for (; t <= stop; t += 2) {
               level(I0{}, PF{}, M2{}, t);
               level(I1{}, PF{}, M2{}, t + 1);
@@ -810,7 +817,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
             level(I1{}, PF{}, M0{}, t + 1);
           }
         }
-        if (lim < __builtin_huge_val()) {
+        if (HP_ABORT_CODE && lim < __builtin_huge_val()) {
           // Early abort: levels < t are done; stage i has issued
           // nF = (t-1-i)/2 + 1 forwards and nB = (t-2P+i)/2 + 1 backwards
           // (closed form above, every stage past its warm-up). Its remaining
