@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -2600,8 +2601,12 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
   hpk::Bufs b;
   std::vector<Leaf> leaves;
   std::vector<int> hill_ids, exh_ids;
+  const auto t_setup = std::chrono::steady_clock::now();
   hph::Status s = setup_tables(a, p, my_leaves, b, leaves, hill_ids, exh_ids);
   if (!s.ok()) return s;
+  if (std::getenv("HP_DEBUG_TIMING"))
+    std::fprintf(stderr, "search_full: setup_tables %.2f ms (host)\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_setup).count());
   if (a.log.on) {
     a.log.reset();
     a.log.key_of = my_leaves;
@@ -2787,6 +2792,7 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     const int n = static_cast<int>(climb.size());
     hpk::Bufs bh = b;
     bh.nb_rows = b.log.vals == nullptr ? 1 : 0;  // the screen runs unless the log is recorded
+    if (std::getenv("HP_NB_ROWS_OFF")) bh.nb_rows = 0;  // tuning: screened neighbours recompute their durations
     hpk::k_async_seed<<<(n * 32 + T - 1) / T, T, 0, st>>>(bh, q, d_climb, n);
     // one block per SM: up to 160 KB of tables in shared memory
     const hpk::StagedTables tt = staged(bh, std::getenv("HP_NO_STAGE") ? 0 : 160 * 1024);  // (knob: A/B)
