@@ -72,3 +72,19 @@ def test_closed_form_levels():
                 assert t == (i + m if m < P - i else 2 * m + i), (P, M, i, m)
             for (i, j), t in Bk.items():
                 assert t == 2 * P - 1 - i + 2 * j, (P, M, i, j)
+
+
+def test_gpipe_closed_form_levels():
+    """GPipe (sim.cpp:46-50): F(i,m) at level i+m, B(i,j) at 2P-2-i+M+j, so
+    every forward runs before every backward (levels [0, M+P-2] then
+    [M+P-1, 2M+2P-3]) — the two wavefronts of hp_kernels.cu
+    eval_item_generic's GPipe path."""
+    for P in range(1, 21):
+        for M in range(1, 30):
+            _, T, F, Bk = asap(P, M, True)
+            assert T == 2 * (M + P - 1)
+            for (i, m), t in F.items():
+                assert t == i + m, (P, M, i, m)
+            for (i, j), t in Bk.items():
+                assert t == 2 * P - 2 - i + M + j, (P, M, i, j)
+            assert max(F.values()) < min(Bk.values())
