@@ -166,6 +166,14 @@ __device__ inline void simulate_list(const Bufs& b, int li, int kind, const long
   }
 }
 
+// HP_DEBUG_TASKS phase accounting: cycles since the last mark go to `acc`.
+#define DBG_MARK(acc)                  \
+  if (b.trace) {                       \
+    const long long now_ = clock64();  \
+    acc += now_ - dbg_c;               \
+    dbg_c = now_;                      \
+  }
+
 // One block of DEF_WARPS warps per task, tasks pulled in `order` (longest
 // expected first). The task's leaves run in reference order; per leaf every
 // batch (the seeds, a hill-climb neighbourhood, a chunk of exhaustive
@@ -213,16 +221,12 @@ __global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs bg, const TaskDev*
     const double gb = probe ? INF : __longlong_as_double(*(volatile long long*)gb_bits);
     int lseq = 0;  // search-log segment counter of this task (thread 0)
     const bool logging = b.log.vals != nullptr && !probe;
-    // HP_DEBUG_TASKS: per task (cycles, leaves, hill steps, simulations)
+    // HP_DEBUG_TASKS (thread 0's view): per task total cycles, leaves, hill
+    // steps, simulations, and cycles per phase (seeds, simulation, gates,
+    // replay, memo marks), accumulated at the block's sync points
     const long long dbg_t0 = b.trace ? clock64() : 0;
     long long dbg_steps = 0;
     long long dbg_sim = 0, dbg_gate = 0, dbg_rep = 0, dbg_seed = 0, dbg_c = 0, dbg_mo = 0;
-#define DBG_MARK(acc)                  \
-  if (b.trace) {                       \
-    const long long now_ = clock64();  \
-    acc += now_ - dbg_c;               \
-    dbg_c = now_;                      \
-  }
     if (b.trace) dbg_c = clock64();
 
     // ---- seeds of every leaf and their gates (incumbent-free)
@@ -574,3 +578,5 @@ __global__ void __launch_bounds__(DEF_THREADS) k_default(Bufs bg, const TaskDev*
     __syncthreads();
   }
 }
+
+#undef DBG_MARK
