@@ -1100,9 +1100,12 @@ __device__ void lb_scan_warp(const Leaf& lf, StageLB* s, int lane) {
       dps[r] = __ldcg(&s[i].dps);
       sa = sa + f[r] + sf[r];
       sb = sb + sf[r] + bk[r];
+    } else {
+      f[r] = bk[r] = sf[r] = dps[r] = 0.0;
     }
   }
   double A = warp_excl_sum(sa, lane), Bt = warp_excl_sum(sb, lane);
+  const double Bt0 = Bt;
   double mx = neg_inf(), my = neg_inf();
   double X[8], Y[8];
 #pragma unroll
@@ -1141,6 +1144,57 @@ __device__ void lb_scan_warp(const Leaf& lf, StageLB* s, int lane) {
       sy = dmax(sy, Y[r]);
       __stcg(&s[i].SX, sx);
       __stcg(&s[i].SY, sy);
+    }
+  }
+  // pair circuits (pair_gain, lb_scan): pair i needs stage i+1's f, b, dps
+  // and Bt_{i+1}; the chunk's last pair takes them from the next lane (whose
+  // chunk starts at Bt_{i1}, this lane's running Bt)
+  const double nf = __shfl_down_sync(0xffffffffu, f[0], 1);
+  const double nbk = __shfl_down_sync(0xffffffffu, bk[0], 1);
+  const double ndps = __shfl_down_sync(0xffffffffu, dps[0], 1);
+  const bool pairs = lf.sched == 1;
+  double gx[8], gy[8];
+  double mg = neg_inf(), mgy = neg_inf();
+  double bt = Bt0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + r;
+    gx[r] = gy[r] = neg_inf();
+    if (i < i1) {
+      const double bt1 = bt + sf[r] + bk[r];  // Bt_{i+1}
+      if (pairs && i + 1 < P) {
+        const bool in = r + 1 < 8 && i + 1 < i1;
+        const double fe = in ? f[r < 7 ? r + 1 : 7] : nf;
+        const double be = in ? bk[r < 7 ? r + 1 : 7] : nbk;
+        const double de = in ? dps[r < 7 ? r + 1 : 7] : ndps;
+        gx[r] = pair_gain(lf.M, P, i, pair_cyc(f[r], bk[r], fe, be, sf[r]), be);
+        gy[r] = gx[r] - bt1 + de;
+      }
+      mg = dmax(mg, gx[r]);
+      mgy = dmax(mgy, gy[r]);
+      bt = bt1;
+    }
+  }
+  double pg = warp_excl_max(mg, lane), pgy = warp_excl_max(mgy, lane);
+  double sg = warp_excl_suffix_max(mg, lane), sgy = warp_excl_suffix_max(mgy, lane);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + r;
+    if (i < i1) {
+      __stcg(&s[i].PG, pg);
+      __stcg(&s[i].PGY, pgy);
+      pg = dmax(pg, gx[r]);
+      pgy = dmax(pgy, gy[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 7; r >= 0; --r) {
+    const int i = i0 + r;
+    if (i < i1) {
+      sg = dmax(sg, gx[r]);
+      sgy = dmax(sgy, gy[r]);
+      __stcg(&s[i].SG, sg);
+      __stcg(&s[i].SGY, sgy);
     }
   }
 }

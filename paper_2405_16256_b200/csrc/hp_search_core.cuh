@@ -245,9 +245,40 @@ struct StageLB {
   double A, Bt;          // sum_{i<k} (f_i + sf_i), sum_{i<k} (sf_i + b_i)
   double PX, PY;         // max_{j<k} X_j, max_{j<k} Y_j
   double SX, SY;         // max_{j>=k} X_j, max_{j>=k} Y_j
+  double PG, PGY;        // max_{j<k} GX_j, max_{j<k} GY_j (pair circuits, pair_gain)
+  double SG, SGY;        // max_{j>=k} GX_j, max_{j>=k} GY_j
 };
 
 HPD double neg_inf() { return -__builtin_huge_val(); }
+
+// Pair-circuit term of the 1F1B bound. On stage k the op after B(k, m) is
+// F(k, m + w_k) (w_k = P - k in-flight, M >= P - k); that forward reaches
+// stage k+1 as F(k+1, (m + 1) + w_{k+1}), which stage k+1 runs right before
+// B(k+1, m + 2). So B(k+1, m) -> B(k, m) -> F(k, m + w_k) -> F(k+1, ...) ->
+// B(k+1, m + 2) is a circuit of length
+//   cyc = f_k + b_k + f_{k+1} + b_{k+1} + 2 sf_k
+// per two microbatches (the link k <-> k+1 carries both sends), taken n
+// times from B(k+1, 0) while F(k, m + w_k) exists. B(k+1, 0) cannot start
+// before microbatch 0's round trip (all forwards, then the backwards of the
+// stages after k+1), and the remaining backwards of stage k+1 and the
+// backward chain to stage 0 follow. Written against T0 = sum of all f, b and
+// sends, the bound of pair k is
+//   T0 + G_k + dps_0            (GX_k = G_k)
+//   T0 + G_k - Bt_{k+1} + dps_{k+1}   (GY_k, the stage's own DP sync)
+// with G_k = n cyc + (M - 1 - 2n) b_{k+1} returned here; -inf when the
+// circuit does not exist (M < P - k). Slow links between two stages make
+// this the binding bound: the per-stage bound misses 2 sf_k / 2 per
+// microbatch of send time the 1F1B alternation cannot overlap.
+HPD double pair_gain(long long M, int P, int k, double cyc, double b_e) {
+  const long long w = P - k;
+  if (M < w) return neg_inf();
+  const long long n = (M - 1 >= w) ? (M - 1 - w) / 2 + 1 : 0;
+  return (double)n * cyc + (double)(M - 1 - 2 * n) * b_e;
+}
+
+HPD double pair_cyc(double fk, double bk, double fe, double be, double sfk) {
+  return ((fk + bk) + (fe + be)) + 2.0 * sfk;
+}
 
 // durations of stage i of the current split (feasible by construction)
 HPD void lb_stage(const Consts& c, const Leaf& lf, const LeafGroup* lg, const uint8_t* slots,
@@ -286,6 +317,79 @@ HPD void lb_scan(const Leaf& lf, StageLB* s) {
     s[k].SX = sx;
     s[k].SY = sy;
   }
+  // pair circuits (pair_gain): GX_k, GY_k for pairs k = 0 .. P-2
+  double pg = neg_inf(), pgy = neg_inf();
+  for (int k = 0; k < P; ++k) {
+    s[k].PG = pg;
+    s[k].PGY = pgy;
+    double gx = neg_inf(), gy = neg_inf();
+    if (k + 1 < P && lf.sched == 1) {
+      gx = pair_gain(lf.M, P, k, pair_cyc(s[k].f, s[k].b, s[k + 1].f, s[k + 1].b, s[k].sf), s[k + 1].b);
+      gy = gx - s[k + 1].Bt + s[k + 1].dps;
+    }
+    s[k].SG = gx;
+    s[k].SGY = gy;
+    pg = dmax(pg, gx);
+    pgy = dmax(pgy, gy);
+  }
+  double sg = neg_inf(), sgy = neg_inf();
+  for (int k = P - 1; k >= 0; --k) {
+    sg = dmax(sg, s[k].SG);
+    sgy = dmax(sgy, s[k].SGY);
+    s[k].SG = sg;
+    s[k].SGY = sgy;
+  }
+}
+
+// T0 = sum of every f, b and send of the current split (pair_gain).
+HPD double lb_total(const Leaf& lf, const StageLB* s) {
+  const int k = lf.P - 1;
+  return (HP_LDX(&s[k].A) + HP_LDX(&s[k].f)) + (HP_LDX(&s[k].Bt) + HP_LDX(&s[k].b));
+}
+
+// Pair-circuit part of the bound of the neighbour that gives stages bb and
+// bb+1 the durations (f0, b0, p0) and (f1, b1, p1): the three pairs that
+// contain a changed stage explicitly, the others through the prefix /
+// suffix maxima shifted by the changed sums (T0 by dA + dB, Bt_{k+1} by dB
+// for k > bb).
+HPD double pair_lb_nb(const Leaf& lf, const StageLB* s, int bb, double f0, double b0, double p0,
+                      double f1, double b1, double p1, double dps0, double dA, double dB) {
+#ifdef HP_NO_PAIR_LB
+  return neg_inf();  // tuning / A-B: per-stage bound only
+#endif
+  if (lf.sched != 1) return neg_inf();
+  const int P = lf.P;
+  const long long M = lf.M;
+  const double T = lb_total(lf, s) + (dA + dB);
+  double g = neg_inf(), gy = neg_inf();
+  if (bb >= 1) {
+    g = HP_LDX(&s[bb - 1].PG);
+    gy = HP_LDX(&s[bb - 1].PGY);
+    // pair (bb-1, bb)
+    const double fk = HP_LDX(&s[bb - 1].f), bk = HP_LDX(&s[bb - 1].b), sfk = HP_LDX(&s[bb - 1].sf);
+    const double G = pair_gain(M, P, bb - 1, pair_cyc(fk, bk, f0, b0, sfk), b0);
+    g = dmax(g, G);
+    gy = dmax(gy, G - HP_LDX(&s[bb].Bt) + p0);
+  }
+  const double sfb = HP_LDX(&s[bb].sf);
+  const double Bt1 = HP_LDX(&s[bb].Bt) + sfb + b0;  // the neighbour's Bt_{bb+1}
+  {
+    // pair (bb, bb+1)
+    const double G = pair_gain(M, P, bb, pair_cyc(f0, b0, f1, b1, sfb), b1);
+    g = dmax(g, G);
+    gy = dmax(gy, G - Bt1 + p1);
+  }
+  if (bb + 2 < P) {
+    // pair (bb+1, bb+2)
+    const double fe = HP_LDX(&s[bb + 2].f), be = HP_LDX(&s[bb + 2].b);
+    const double G = pair_gain(M, P, bb + 1, pair_cyc(f1, b1, fe, be, HP_LDX(&s[bb + 1].sf)), be);
+    g = dmax(g, G);
+    gy = dmax(gy, G - (HP_LDX(&s[bb + 2].Bt) + dB) + HP_LDX(&s[bb + 2].dps));
+    // pairs bb+2 .. P-2
+    g = dmax(g, HP_LDX(&s[bb + 2].SG));
+    gy = dmax(gy, HP_LDX(&s[bb + 2].SGY) - dB);
+  }
+  return dmax(T + g + dps0, T + gy);
 }
 
 // Screens neighbour slot q of `cur` (boundary q >> 1, +1 for even q):
@@ -314,6 +418,11 @@ HPD double nb_screen(const Consts& c, const Leaf& lf, const LeafGroup* lg, const
     const double dA = (d0.f - s[bb].f) + (d1.f - s[bb + 1].f);
     const double dB = (d0.b - s[bb].b) + (d1.b - s[bb + 1].b);
     lb = dmax(lb, dmax(s[bb + 2].SX + dA + dB + dps0, s[bb + 2].SY + dA));
+  }
+  {
+    const double dA = (d0.f - s[bb].f) + (d1.f - s[bb + 1].f);
+    const double dB = (d0.b - s[bb].b) + (d1.b - s[bb + 1].b);
+    lb = dmax(lb, pair_lb_nb(lf, s, bb, d0.f, d0.b, d0.dps, d1.f, d1.b, d1.dps, dps0, dA, dB));
   }
   return lb > cur_t * (1.0 + kScreenMargin) ? T_SKIP : 0.0;
 }
@@ -369,6 +478,7 @@ HPD double nb_lb_pre(const Leaf& lf, const StageLB* s, const StageNb* nbs, int q
   const double dA = (f0 - fbb) + (f1 - fb1);
   const double dB = (b0 - bbb) + (b1 - bb1);
   if (bb + 2 < P) lb = dmax(lb, dmax(HP_LDX(&s[bb + 2].SX) + dA + dB + dps0, HP_LDX(&s[bb + 2].SY) + dA));
+  lb = dmax(lb, pair_lb_nb(lf, s, bb, f0, b0, p0, f1, b1, p1, dps0, dA, dB));
   return dmax(lb, 0.0);
 }
 

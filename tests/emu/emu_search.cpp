@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include <algorithm>
 // TEST HARNESS ONLY — CPU emulation of the GPU search decomposition.
 //
@@ -20,6 +21,8 @@ namespace {
 long long g_screened = 0, g_neighbours = 0;  // nb_screen statistics (T_SKIP / all)
 long long g_screen_mismatch = 0;              // nb_screen_pre != nb_screen (must stay 0)
 long long g_bound_viol = 0;                   // nb_lb_pre above a simulated time (must stay 0)
+int g_check_all = 0;                          // also simulate screened neighbours (emu_check_all)
+long long g_checked = 0;                      // screened neighbours simulated for the check
 
 struct LeafDev {
   Leaf lf;
@@ -71,7 +74,7 @@ extern "C" int emu_search_shard(const hp_problem* in, int shard, int count, hp_r
     const hph::Task& t = p.tasks[h.task];
     LeafDev L;
     L.lf = Leaf{h.task, t.pp, (int)h.M, h.dp, h.B, h.B_idx, t.layout_off, 0, 0,
-                p.uniform_only ? 2 : (h.exhaustive ? 1 : 0), 0};
+                p.uniform_only ? 2 : (h.exhaustive ? 1 : 0), p.schedule};
     for (int g = 0; g < G; ++g)
       L.lg.push_back(hph::leaf_group(p, g, hph::leaf_tp(p, h, g), h.B, h.dp, hph::leaf_nodes(p, h, g)));
     L.slots = &p.layouts[t.layout_off];
@@ -116,12 +119,34 @@ extern "C" int emu_search_shard(const hp_problem* in, int shard, int count, hp_r
         lb_scan(L.lf, slb.data());
         for (int q = 0; q < 2 * (P - 1); ++q) {
           const double lbq = nb_lb_pre(L.lf, slb.data(), snb.data(), q);
+          if (getenv("EMU_DBG") && q < 4) {
+            int b = q >> 1, d = (q & 1) ? -1 : 1;
+            const int k0 = (q & 1) ? 0 : 1, k1 = 1 - k0;
+            const double dA = (snb[b].f[k0] - slb[b].f) + (snb[b + 1].f[k1] - slb[b + 1].f);
+            const double dB = (snb[b].b[k0] - slb[b].b) + (snb[b + 1].b[k1] - slb[b + 1].b);
+            double pl = pair_lb_nb(L.lf, slb.data(), b, snb[b].f[k0], snb[b].b[k0], snb[b].dps[k0], snb[b + 1].f[k1],
+                                   snb[b + 1].b[k1], snb[b + 1].dps[k1], b == 0 ? snb[0].dps[k0] : slb[0].dps, dA, dB);
+            printf("q %d lb %.9g pair %.9g cur %.9g T0 %.9g PG %.3g SG %.3g sched %d\n", q, lbq, pl, hs.cur_time,
+                   lb_total(L.lf, slb.data()), slb[b + 2 < P ? b + 2 : 0].SG, slb[0].SG, L.lf.sched);
+            (void)d;
+          }
           lbv[q] = lbq;
           double scr = screen_of(lbq, hs.cur_time);
           double ref = nb_screen(c, L.lf, L.lg.data(), L.slots, L.hop, cur.data(), slb.data(), q, hs.cur_time);
           if (!(scr == ref)) g_screen_mismatch++;
           g_neighbours++;
           if (scr == T_SKIP) g_screened++;
+          if (scr == T_SKIP && g_check_all) {
+            // admissibility of the screen itself: a screened neighbour's
+            // simulated time must not be below its bound
+            int b = q >> 1, d = (q & 1) ? -1 : 1;
+            tmp = cur;
+            tmp[b] += d; tmp[b + 1] -= d;
+            const double t = eval(c, L, tmp.data());
+            g_checked++;
+            if (t >= 0 && lbq > t * (1.0 + 1e-9)) g_bound_viol++;
+            if (t >= 0 && !(t > hs.cur_time)) g_bound_viol++;
+          }
           if (scr != 0.0) {
             nb[q] = scr;
             continue;
@@ -164,6 +189,7 @@ extern "C" void emu_screen_stats(long long* screened, long long* neighbours, int
 
 extern "C" long long emu_screen_mismatches() { return g_screen_mismatch; }
 extern "C" long long emu_bound_violations() { return g_bound_viol; }
+extern "C" long long emu_check_all(int on) { g_check_all = on; return g_checked; }
 
 // Explicit-plan evaluation through the same per-stage setup + serial
 // level-synchronous simulation (mode 3 pseudo-leaf, like hp_evaluate_plans).

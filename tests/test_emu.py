@@ -54,6 +54,29 @@ def test_emu_matches_reference_full_mode(search_cases, emu):
     assert emu.emu_bound_violations() == 0
 
 
+def test_emu_screen_is_admissible(search_cases, emu):
+    """Every neighbour the screen skips (per-stage and pair-circuit bounds,
+    hp_search_core.cuh) is simulated anyway here: its time is never below
+    its bound, and it is strictly above the climb point, so skipping it
+    cannot change a move, a tie or a count."""
+    emu.emu_check_all.restype = C.c_longlong
+    emu.emu_bound_violations.restype = C.c_longlong
+    before = emu.emu_check_all(1)
+    v0 = emu.emu_bound_violations()
+    try:
+        for case in full_cases(search_cases):
+            if case["status"] == 2:
+                continue
+            p = abi.Problem(case["docs"])
+            res = abi.hp_result()
+            assert emu.emu_search(C.byref(p.struct), C.byref(res)) == abi.HP_OK
+            assert hexbits(res.best_time_s) == case["iteration_bits"], case["name"]
+    finally:
+        checked = emu.emu_check_all(0) - before
+    assert checked > 1000
+    assert emu.emu_bound_violations() == v0
+
+
 def test_emu_shards_partition_the_leaves(search_cases, emu):
     """Leaf shards are disjoint and cover the space: per-shard counts add up
     and the exact reduction (hp_better_than) picks the unsharded plan."""
