@@ -121,6 +121,7 @@ extern "C" int lb_analysis(const hp_problem* in, int sample_every, int max_pm) {
   std::vector<double> hop = hph::hop_table(p);
   double work_all = 0, work_skip = 0, n_all = 0, n_skip = 0;
   double lb_gap_sum = 0; long gap_n = 0;
+  static int surv_dumped = 0;
   double work_skip2 = 0, n_skip2 = 0, work_worse = 0, n_worse = 0;
   printf("leaves %zu\n", p.leaves.size());
   if (getenv("LBP_J")) g_J = atoi(getenv("LBP_J"));
@@ -183,6 +184,15 @@ extern "C" int lb_analysis(const hp_problem* in, int sample_every, int max_pm) {
         if (lbs[q] > ct * (1 + 1e-9)) { work_skip += wk; n_skip += 1; }
         if (lbs2[q] > ct * (1 + 1e-9)) { work_skip2 += wk; n_skip2 += 1; }
         if (nb[q] > ct * (1 + 1e-9)) { work_worse += wk; n_worse += 1; }
+        if (getenv("LBP_SURV") && nb[q] > ct * (1 + 1e-9) && !(lbs2[q] > ct * (1 + 1e-9)) &&
+            (nb[q] - lbs2[q]) / nb[q] > 0.015 && !surv_dumped++) {
+          tmp = cur; tmp[q >> 1] += (q & 1) ? -1 : 1; tmp[(q >> 1) + 1] -= (q & 1) ? -1 : 1;
+          eval(tmp.data(), nullptr);
+          FILE* fo = fopen(getenv("LBP_SURV"), "w");
+          fprintf(fo, "%d %lld %.17g %.17g %.17g\n", P, (long long)lf.M, ct, nb[q], lbs2[q]);
+          for (int i = 0; i < P; ++i) fprintf(fo, "%.17g %.17g %.17g %.17g %.17g\n", d[i].f, d[i].b, d[i].sf, d[i].sb, d[i].dps);
+          fclose(fo);
+        }
         if (getenv("LBP_DUMP") && nb[q] > ct * (1 + 1e-9) && !(lbs2[q] > ct * (1 + 1e-9)))
           printf("W q=%d bb=%d P=%d M=%lld worse %.3e gap %.3e\n", q, q >> 1, P, (long long)lf.M, (nb[q] - ct) / ct, (nb[q] - lbs2[q]) / nb[q]);
         if (lbs2[q] > nb[q] * (1 + 1e-12)) { printf("INADMISSIBLE rt lb %.17g > t %.17g\n", lbs2[q], nb[q]); return 2; }
