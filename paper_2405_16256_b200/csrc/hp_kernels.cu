@@ -2797,7 +2797,13 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     q.active = reinterpret_cast<int*>(d_q + 6);
     q.progress = d_q + 7;
     q.cap = qcap;
-    q.hi_levels = 1LL << 17;
+    // a leaf moves to ring 1 once its climb has run 4096 levels (the third
+    // step of a P = 96, M = 1536 climb): continuing climbs go before the
+    // first steps still queued, which shortens every long chain. C3 full,
+    // 2 alternating runs per value (2^17 -> 4096): 1 GPU 198.1 -> 192.1 ms,
+    // 2 GPUs 126.5 -> 121.8, 4 GPUs 93.8 -> 89.5; 0 (one ring for all):
+    // 2 GPUs 126.8.
+    q.hi_levels = 4096;
     q.r1_thr = -1;  // set below from the grid (one item per SM of backlog)
     if (const char* e = std::getenv("HP_R1_THR")) q.r1_thr = std::max(0, std::atoi(e));  // tuning
     q.r0_thr = -1;

@@ -10,7 +10,15 @@ if ":" in name and name.startswith("C3"):
     cfg = configs.with_pp(configs.config(base, full=full), [int(x) for x in pps.split(",")])
 else:
     cfg = configs.config(name, full=full)
+shard = os.environ.get("RUN_SHARD")  # "r/n": one shard of an n-GPU sweep on this GPU
 for _ in range(reps):
+    if shard:
+        r, n = (int(x) for x in shard.split("/"))
+        eng = planner.Engine(0)
+        t0 = time.time(); res = eng.search_shard(abi.Problem(cfg), r, n); t1 = time.time()
+        print(json.dumps({"cfg": name, "shard": shard, "wall_s": t1 - t0, "dev_ms": res.device_ms,
+                          "sim": res.candidates_simulated}), flush=True)
+        continue
     t0 = time.time(); o = planner.search(cfg); t1 = time.time()
     print(json.dumps({"cfg": name, "wall_s": t1 - t0, "dev_ms": o.device_ms, "sim": o.candidates_simulated,
                       "pruned": o.candidates_pruned, "t": o.iteration_time_s, "launches": o.gpu_launches,
