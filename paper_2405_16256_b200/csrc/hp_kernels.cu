@@ -328,7 +328,6 @@ __device__ __forceinline__ void eval_item_generic(const Bufs& b, const Work& w, 
         if (j == P - 1) {
           v = rem;
         } else {
-          int left = P - j;
           for (v = 1;; ++v) {
             long long cntv = exh_count(b, lf, w.leaf, j, rem, v);
             if (rank < cntv) break;
@@ -530,7 +529,6 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
       if (j == P - 1) {
         v = rem;
       } else {
-        int left = P - j;
         for (v = 1;; ++v) {
           long long cntv = exh_count(b, lf, w.leaf, j, rem, v);
           if (rank < cntv) break;
@@ -1857,8 +1855,6 @@ __global__ void k_exh_reduce(Bufs b, const ExhSpan* spans, int n_spans) {
   if (k >= n_spans) return;
   const ExhSpan sp = spans[k];
   const Leaf lf = b.leaves[sp.leaf];
-  const LeafGroup* lg = b.lg + lf.lg_off;
-  const uint8_t* slots = b.layouts + lf.layout_off;
   HillState hs = b.hs[sp.leaf];
   int* best = b.best + lf.split_off;
   int comp[HP_MAX_STAGES];
@@ -2698,7 +2694,6 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
 
   // ---- seed evaluation (uniform + proportional of hill / uniform-only leaves)
   std::vector<std::vector<Work>> seedq(hpk::NCLS);
-  const bool gpipe = p.schedule == HP_GPIPE;
   for (int k : hill_ids) {
     int cls = hpk::eval_class(leaves[k].P, leaves[k].M, leaves[k].sched == 0);
     int cpw = hpk::class_cpw(cls, leaves[k].P);

@@ -86,6 +86,7 @@ static double lower_bound_cyc(const Consts& c, const Leaf& lf, const StageDur* d
 // length C = sum_{i=k}^{k+j} (f_i + b_i) + the sends between them, taken
 // once per j+1 microbatches (w_k = w_{k+j} + j while M >= P - k).
 static int g_J = 1;
+static long g_rank[9], g_prank[9];
 static double lower_bound_win(const Consts& c, const Leaf& lf, const StageDur* d) {
   const int P = lf.P;
   const long long M = lf.M;
@@ -155,6 +156,8 @@ extern "C" int lb_analysis(const hp_problem* in, int sample_every, int max_pm) {
     double tu = eval(uni.data(), nullptr), tp = eval(prop.data(), nullptr);
     hill_init(c, lf, lg.data(), slots, uni.data(), prop.data(), tu, tp, cur.data(), bs.data(), hs, false);
     std::vector<double> lbs(2 * P);
+    std::vector<double> prev_t;
+    int prev_move = -1;
     static int dumped = 0;
     if (getenv("LBP_STAGES") && hs.active && lf.M >= 1000 && !dumped++) {
       eval(cur.data(), nullptr);
@@ -199,6 +202,32 @@ extern "C" int lb_analysis(const hp_problem* in, int sample_every, int max_pm) {
         lb_gap_sum += nb[q] / lbs[q]; gap_n++;
         if (lbs[q] > nb[q] * (1 + 1e-12)) { printf("INADMISSIBLE lb %.17g > t %.17g\n", lbs[q], nb[q]); return 2; }
       }
+      {
+        // move prediction: rank of the steepest move among the neighbours by bound
+        int bq = -1;
+        for (int q = 0; q < 2 * (P - 1); ++q)
+          if (nb[q] >= 0 && (bq < 0 || nb[q] < nb[bq])) bq = q;
+        if (bq >= 0 && nb[bq] < ct) {
+          // rank of this move among the previous step's neighbours by time
+          if (!prev_t.empty()) {
+            int pr = 0;
+            const double tm = prev_t[bq];
+            if (tm < 0) pr = 8;
+            else for (int q = 0; q < 2 * (P - 1); ++q)
+              if (q != prev_move && prev_t[q] >= 0 && q != bq && (prev_t[q] < tm || (prev_t[q] == tm && q < bq))) pr++;
+            g_prank[pr < 8 ? pr : 8]++;
+          }
+          if (getenv("LBP_MOVES") && li == 0 + atoi(getenv("LBP_MOVES"))) printf("M %d %.3e %.3e\n", bq, (ct - nb[bq]) / ct, prev_t.empty() ? 0.0 : prev_t[bq]);
+          prev_t.assign(nb.begin(), nb.begin() + 2 * (P - 1));
+          prev_move = bq;
+          int rank = 0;
+          for (int q = 0; q < 2 * (P - 1); ++q)
+            if (nb[q] >= 0 && q != bq && (lbs2[q] < lbs2[bq] || (lbs2[q] == lbs2[bq] && q < bq))) rank++;
+          g_rank[rank < 7 ? rank : 7]++;
+        } else {
+          g_rank[8]++;
+        }
+      }
       std::fill(dl.begin(), dl.end(), 0);
       hill_step(c, lf, lg.data(), slots, cur.data(), uni.data(), prop.data(), bs.data(), hist.data(), hs,
                 nb.data(), delta.data(), old.data(), tmp.data());
@@ -206,6 +235,12 @@ extern "C" int lb_analysis(const hp_problem* in, int sample_every, int max_pm) {
   }
   printf("neighbours %.0f skip %.0f (%.1f%%), work skip %.1f%%, mean t/lb %.4f\n", n_all, n_skip,
          100 * n_skip / n_all, 100 * work_skip / work_all, lb_gap_sum / gap_n);
+  printf("move rank among the previous step's neighbours by time (0..7, >=8):");
+  for (int r = 0; r < 9; ++r) printf(" %ld", g_prank[r]);
+  printf("\n");
+  printf("move rank by bound (0..6, >=7, no move):");
+  for (int r = 0; r < 9; ++r) printf(" %ld", g_rank[r]);
+  printf("\n");
   printf("round-trip bound: skip %.0f (%.1f%%), work skip %.1f%%; strictly worse (ceiling) %.0f (%.1f%%), work %.1f%%\n",
          n_skip2, 100 * n_skip2 / n_all, 100 * work_skip2 / work_all, n_worse, 100 * n_worse / n_all,
          100 * work_worse / work_all);
