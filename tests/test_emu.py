@@ -77,6 +77,41 @@ def test_emu_screen_is_admissible(search_cases, emu):
     assert emu.emu_bound_violations() == v0
 
 
+def test_emu_climb_cases_screen(emu):
+    """The climb-heavy, slow-link instances (tests/golden/climb_cases.json):
+    the emulated GPU search equals the reference, the pair-circuit term
+    screens neighbours the per-stage bound keeps, and every screened
+    neighbour, simulated anyway, is strictly worse than the climb point."""
+    from conftest import load_golden
+    emu.emu_check_all.restype = C.c_longlong
+    emu.emu_bound_violations.restype = C.c_longlong
+    sk, nn = C.c_longlong(), C.c_longlong()
+    emu.emu_screen_stats(C.byref(sk), C.byref(nn), 1)
+    before = emu.emu_check_all(1)
+    v0 = emu.emu_bound_violations()
+    n = 0
+    try:
+        for case in load_golden("climb_cases.json")["cases"]:
+            p = abi.Problem(case["docs"])
+            res = abi.hp_result()
+            st = emu.emu_search(C.byref(p.struct), C.byref(res))
+            if case["status"] != 0:
+                assert st != abi.HP_OK, case["name"]
+                continue
+            assert st == abi.HP_OK, case["name"]
+            assert hexbits(res.best_time_s) == case["iteration_bits"], case["name"]
+            assert (res.candidates_simulated, res.candidates_pruned) == (
+                case["candidates_simulated"], case["candidates_pruned"]), case["name"]
+            n += 1
+    finally:
+        checked = emu.emu_check_all(0) - before
+    emu.emu_screen_stats(C.byref(sk), C.byref(nn), 1)
+    assert n >= 50
+    assert emu.emu_bound_violations() == v0
+    # 129,096 of 899,094 neighbours with the per-stage bound alone
+    assert checked == sk.value and sk.value > 200000, (checked, sk.value, nn.value)
+
+
 def test_emu_shards_partition_the_leaves(search_cases, emu):
     """Leaf shards are disjoint and cover the space: per-shard counts add up
     and the exact reduction (hp_better_than) picks the unsharded plan."""

@@ -158,6 +158,18 @@ def test_c4_c5_against_reference(engine):
             assert h.hexdigest() == case["log"]["sha256"], case["name"]
 
 
+def test_climb_cases_against_reference(engine):
+    """60 full-sweep instances where the hill climb does the work and slow
+    (often cpu-staged) links join the groups, so the neighbour screen's
+    per-stage and pair-circuit bounds skip most neighbours: plan, time bits
+    and counts equal the compiled reference's (tests/golden/gen_climb_cases.py)."""
+    from conftest import load_golden
+    cases = load_golden("climb_cases.json")["cases"]
+    assert len(cases) == 60 and sum(c["status"] == 0 for c in cases) >= 50
+    for case in cases:
+        check_case(engine, case)
+
+
 def test_gpipe_search_at_scale(engine):
     """GPipe search at P*M up to 98,304 (C3, pp 64, micro-batch 1, memory
     unbounded): the generic evaluator in the climb kernel against the
