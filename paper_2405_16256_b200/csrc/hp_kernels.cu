@@ -1296,15 +1296,84 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
   hs.steps = __ldcg(&b.hs[li].steps);
   hs.has_best = __ldcg(&b.hs[li].has_best);
   constexpr int NK = (HP_MAX_STAGES + 31) / 32;
+  // Everything the step reads is loaded up front in one round of independent
+  // L2 loads (the leaf's state was written by whichever SM ran the previous
+  // step): the neighbour times, this lane's chunk of the current split, and
+  // the newest 32 * BV path points' move codes and memo distances. Only a
+  // climb longer than the window reads its older points chunk by chunk.
+  const int C = (P + 31) >> 5;
+  const int i0 = min(P, lane * C), i1 = min(P, i0 + C);
+  double nv[NK][2];
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    const int bb = lane + 32 * k;
+    nv[k][0] = nv[k][1] = T_INVALID;
+    if (bb + 1 < P) {
+      nv[k][0] = __ldcg(nb + 2 * bb);
+      nv[k][1] = __ldcg(nb + 2 * bb + 1);
+    }
+  }
+  int cv[8];  // cur[i0 + r] (C <= 8)
+#pragma unroll
+  for (int r = 0; r < 8; ++r) cv[r] = i0 + r < i1 ? __ldcg(cur + i0 + r) : 0;
+  long long g_sim = 0, g_pru = 0;
+  if (lane == 0) {
+    g_sim = __ldcg(&b.hs[li].simulated);
+    g_pru = __ldcg(&b.hs[li].pruned);
+  }
+  int* memo = b.memo_d + b.hist_off[li];
+  constexpr int BV = 16;
+  const int top = hs.steps - 1;
+  int hv[BV], dv[BV];  // point top - 32 v - lane: move code, D
+#pragma unroll
+  for (int v = 0; v < BV; ++v) {
+    const int idx = top - 32 * v - lane;
+    hv[v] = idx >= 0 ? __ldcg(hist + idx) : 0;
+    dv[v] = idx >= 0 ? __ldcg(memo + idx) : 3;
+  }
 
   // ---- mark_old (hp_search_core.cuh): path points t with D_t = ||S_k - S_t||_1
   // <= 2 (memo_d, maintained incrementally below). For those the nonzero
   // boundaries of S_k - S_t come from undoing moves k-1..t (rare beyond t =
   // k-2 on a strictly improving path).
-  int* memo = b.memo_d + b.hist_off[li];
   unsigned oldm = 0;  // bit 2k + (dir < 0) for my boundary lane + 32k
   bool all_old = false;
-  for (int t1 = hs.steps - 1; t1 >= 0; t1 -= 128) {
+#pragma unroll
+  for (int v = 0; v < BV; ++v) {
+    if (top - 32 * v < 0) break;
+    unsigned fl = __ballot_sync(FULL, dv[v] <= 2);
+    while (fl) {
+      const int j = __ffs(fl) - 1;
+      fl &= fl - 1;
+      const int t = top - 32 * v - j;
+      if (__shfl_sync(FULL, dv[v], j) == 0) {
+        all_old = true;
+        continue;
+      }
+      int dl[NK];
+#pragma unroll
+      for (int k = 0; k < NK; ++k) dl[k] = 0;
+      for (int u = top; u >= t; --u) {
+        const int off = top - u, vv = off >> 5;
+        int x = 0;
+#pragma unroll
+        for (int w = 0; w < BV; ++w)
+          if (w == vv) x = hv[w];
+        const int code = __shfl_sync(FULL, x, off & 31);
+        const int bb = code >> 1;
+        if ((bb & 31) == lane) {
+          const int r = bb >> 5;
+#pragma unroll
+          for (int k = 0; k < NK; ++k)
+            if (k == r) dl[k] += (code & 1) ? -1 : 1;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NK; ++k)
+        if (dl[k] != 0) oldm |= 1u << (2 * k + (dl[k] > 0 ? 1 : 0));  // toward c_t
+    }
+  }
+  for (int t1 = top - 32 * BV; t1 >= 0; t1 -= 128) {  // beyond the window
    int dvs[4];
 #pragma unroll
    for (int u = 0; u < 4; ++u) {
@@ -1314,21 +1383,21 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
 #pragma unroll
    for (int u = 0; u < 4; ++u) {
     const int t0 = t1 - 32 * u;
-    const int dv = dvs[u];
-    unsigned fl = __ballot_sync(FULL, dv <= 2);
+    const int dvu = dvs[u];
+    unsigned fl = __ballot_sync(FULL, dvu <= 2);
     while (fl) {
       const int j = __ffs(fl) - 1;
       fl &= fl - 1;
       const int t = t0 - j;
-      if (__shfl_sync(FULL, dv, j) == 0) {
+      if (__shfl_sync(FULL, dvu, j) == 0) {
         all_old = true;
         continue;
       }
       int dl[NK];
 #pragma unroll
       for (int k = 0; k < NK; ++k) dl[k] = 0;
-      for (int u = hs.steps - 1; u >= t; --u) {
-        const int code = __ldcg(hist + u);
+      for (int u2 = top; u2 >= t; --u2) {
+        const int code = __ldcg(hist + u2);
         const int bb = code >> 1;
         if ((bb & 31) == lane) {
           const int r = bb >> 5;
@@ -1345,12 +1414,14 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
   }
   // seeds at distance 1: prefix sums of cur - ref over each lane's chunk
   {
-    const int C = (P + 31) >> 5;
-    const int i0 = min(P, lane * C), i1 = min(P, i0 + C);
     for (int sd = 0; sd < 2; ++sd) {
       const int* ref = (sd == 0 ? b.uni : b.prop) + lf.split_off;
+      int rv[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) rv[r] = i0 + r < i1 ? ref[i0 + r] : 0;
       int loc = 0;
-      for (int i = i0; i < i1; ++i) loc += __ldcg(cur + i) - ref[i];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) loc += cv[r] - rv[r];
       int x = loc;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -1360,12 +1431,16 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
       int e = __shfl_up_sync(FULL, x, 1);
       if (lane == 0) e = 0;
       int dist = 0, cb = -1, cd = 0;
-      for (int i = i0; i < i1 && i + 1 < P; ++i) {
-        e += __ldcg(cur + i) - ref[i];
-        if (e != 0) {
-          dist += abs(e);
-          cb = i;
-          cd = e;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = i0 + r;
+        if (i < i1 && i + 1 < P) {
+          e += cv[r] - rv[r];
+          if (e != 0) {
+            dist += abs(e);
+            cb = i;
+            cd = e;
+          }
         }
       }
       dist = __reduce_add_sync(FULL, dist);
@@ -1391,7 +1466,7 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
 #pragma unroll
       for (int sd = 0; sd < 2; ++sd) {
         const int q = 2 * bb + sd;
-        const double t = __ldcg(nb + q);
+        const double t = nv[k][sd];
         if (t == T_INVALID) continue;
         const bool old = all_old || ((oldm >> (2 * k + sd)) & 1u);
         if (!old) {
@@ -1491,32 +1566,40 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
     __syncwarp();
   } else if (take_n) {
     const int bq = nq >> 1, d = (nq & 1) ? -1 : 1;
-    for (int i = lane; i < P; i += 32) __stcg(best + i, __ldcg(cur + i) + (i == bq ? d : (i == bq + 1 ? -d : 0)));
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int i = i0 + r;
+      if (i < i1) __stcg(best + i, cv[r] + (i == bq ? d : (i == bq + 1 ? -d : 0)));
+    }
     hs.has_best = 1;
     hs.best_time = nt;
   }
   __syncwarp();
-  int active = 1;
+  // (warp-uniform after the reductions)
+  int active = (mq == 0x7fffffff || !(mt < hs.cur_time)) ? 0 : 1;  // no feasible neighbour, or no improvement
+  if (active) {
+    // the move: the owner lanes of stages bq, bq + 1 update cur
+    const int bq = mq >> 1, d = (mq & 1) ? -1 : 1;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int i = i0 + r;
+      if (i < i1 && (i == bq || i == bq + 1)) __stcg(cur + i, cv[r] + (i == bq ? d : -d));
+    }
+    if (hs.steps + 1 >= 4 * c_consts.L) active = 0;
+  }
   if (lane == 0) {
     HillState& g = b.hs[li];
-    __stcg(&g.simulated, __ldcg(&g.simulated) + sim);
-    __stcg(&g.pruned, __ldcg(&g.pruned) + pru);
+    __stcg(&g.simulated, g_sim + sim);
+    __stcg(&g.pruned, g_pru + pru);
     __stcg(&g.has_best, hs.has_best);
     __stcg(&g.best_time, hs.best_time);
-    if (mq == 0x7fffffff || !(mt < hs.cur_time)) {  // no feasible neighbour, or no improvement
-      active = 0;
-    } else {
-      const int bq = mq >> 1, d = (mq & 1) ? -1 : 1;
-      __stcg(cur + bq, __ldcg(cur + bq) + d);
-      __stcg(cur + bq + 1, __ldcg(cur + bq + 1) - d);
+    if (!(mq == 0x7fffffff || !(mt < hs.cur_time))) {
       __stcg(hist + hs.steps, (short)mq);
       __stcg(&g.steps, hs.steps + 1);
       __stcg(&g.cur_time, mt);
-      if (hs.steps + 1 >= 4 * c_consts.L) active = 0;
     }
     __stcg(&g.active, active);
   }
-  active = __shfl_sync(FULL, active, 0);
   moved = mq >> 1;
   if (active) {
     // D_t(k+1) = D_t(k) + |c(t) + d| - |c(t)|, c(t) = sum of the moves of
@@ -1524,7 +1607,21 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
     // D_k(k+1) = 1
     const int mb = mq >> 1, md = (mq & 1) ? -1 : 1;
     int carry = 0;
-    for (int t1 = hs.steps - 1; t1 >= 0; t1 -= 128) {
+#pragma unroll
+    for (int v = 0; v < BV; ++v) {
+      if (top - 32 * v < 0) break;
+      const int idx = top - 32 * v - lane;
+      int x = (idx >= 0 && (hv[v] >> 1) == mb) ? ((hv[v] & 1) ? -1 : 1) : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      const int c = carry + x;
+      if (idx >= 0) __stcg(memo + idx, dv[v] + abs(c + md) - abs(c));
+      carry = __shfl_sync(FULL, c, 31);
+    }
+    for (int t1 = top - 32 * BV; t1 >= 0; t1 -= 128) {  // beyond the window
       int xs[4], ms[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
