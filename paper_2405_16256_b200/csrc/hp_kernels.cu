@@ -986,6 +986,10 @@ struct AsyncQ {
   int r1_thr;                   // see pop_item (0: every warp serves ring 1)
   int r0_thr;                   // < 0: ring 0 only on lead warps; else also on the others while
                                 // its backlog exceeds r0_thr
+  int crit_mode;                // with crit_sms: 0 warps 0-3 of those blocks serve ring 0 first,
+                                // then the others, warps 4-7 exit; 1 warps 0-3 serve ring 0
+                                // only, warps 4-7 the other rings; 2 warps 0-3 ring 0 only,
+                                // warps 4-7 exit
 };
 
 __device__ __forceinline__ int leaf_class(const Leaf& lf) { return eval_class(lf.P, lf.M, lf.sched == 0); }
@@ -1760,7 +1764,8 @@ __device__ __forceinline__ int try_slot(const AsyncQ& q, int lv, unsigned long l
 // anything else, so it stays unread for at most the one item in progress
 // when it was filled. Returns false when the warp should exit (no leaf
 // climbing, or abort).
-__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int lv0, bool lead) {
+__device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int lv0, bool lead,
+                         int lv_end = kRings) {
   unsigned ns = 32;
   long long t0 = clock64();
   unsigned long long seen = *(volatile unsigned long long*)q.progress;
@@ -1787,7 +1792,7 @@ __device__ bool pop_item(const AsyncQ& q, Work& w, long long (&tk)[kRings], int 
         *(volatile unsigned long long*)q.tail[0] - *(volatile unsigned long long*)q.head[0] >
             (unsigned long long)q.r0_thr)
       lv_start = 0;  // a deep critical backlog: help it
-    for (int lv = lv_start; lv < kRings && !held; ++lv) {
+    for (int lv = lv_start; lv < lv_end && !held; ++lv) {
       const unsigned long long tl = *(volatile unsigned long long*)q.tail[lv];
       const unsigned long long hd = *(volatile unsigned long long*)q.head[lv];
       // (r1_thr > 0: a non-lead warp takes a long-climber item only from a
@@ -1864,7 +1869,8 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
   const Bufs b = stage_tables(bg, tt, smem_tables, &tables_bar);
   const int lane = threadIdx.x & 31;
   long long tk[kRings] = {-1, -1, -1};
-  if (q.crit_sms > 0 && (int)blockIdx.x < q.crit_sms && (threadIdx.x >> 5) >= 4) return;
+  const bool crit_blk = q.crit_sms > 0 && (int)blockIdx.x < q.crit_sms;
+  if (crit_blk && (threadIdx.x >> 5) >= 4 && q.crit_mode != 1) return;
   for (;;) {
     int quit = 0, cls = 0;
     Work w{};
@@ -1874,8 +1880,9 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
       // waits for its slowest item
       const int wib = threadIdx.x >> 5;
       int lv0 = wib < 4 || !q.lead ? 0 : 1;
-      if (q.crit_sms > 0) lv0 = (int)blockIdx.x < q.crit_sms ? 0 : 1;
-      quit = pop_item(q, w, tk, lv0, wib < 4) ? 0 : 1;
+      if (q.crit_sms > 0) lv0 = crit_blk && wib < 4 ? 0 : 1;
+      const int lv_end = crit_blk && wib < 4 && q.crit_mode != 0 ? 1 : kRings;
+      quit = pop_item(q, w, tk, lv0, wib < 4, lv_end) ? 0 : 1;
       if (!quit) cls = w.out > 0 ? w.out - 1 : leaf_class(b.leaves[w.leaf]);
     }
     quit = __shfl_sync(0xffffffffu, quit, 0);
@@ -2919,6 +2926,12 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
       q.crit_sms = a.shard_count >= 4 ? grid / 2 : 0;
       if (const char* e = std::getenv("HP_CRIT_SMS")) q.crit_sms = std::min(grid, std::max(0, std::atoi(e)));  // tuning
       if (q.crit_sms > 0) q.lead = 1;
+      // ... and those SMs' warps 0-3 serve ring 0 only, so a critical item
+      // never waits behind a bulk item there, while warps 4-7 run bulk
+      // (C3 on 4 GPUs, 2 alternating runs: mode 0 89.5 ms, 1 87.4, 2 105.0;
+      // 2 GPUs with the reservation in mode 1: 124.0 -> 123.2, not adopted)
+      q.crit_mode = 1;
+      if (const char* e = std::getenv("HP_CRIT_MODE")) q.crit_mode = std::atoi(e);  // tuning
       long long budget = (long long)(q.crit_sms > 0 ? q.crit_sms : grid) * (q.lead ? 4 : threads / 32);
       if (const char* e = std::getenv("HP_CRIT_WARPS")) budget = std::atoll(e);  // tuning
       std::vector<int> byest(climb);

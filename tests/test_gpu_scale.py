@@ -88,6 +88,8 @@ SCHED_KNOBS = [
     {"HP_CRIT_WARPS": "100000", "HP_HI_LEVELS": "1"},  # (almost) everything prioritised
     {"HP_ASYNC_THREADS": "128"},                 # 4 warps per block
     {"HP_CRIT_SMS": "37"},                       # critical ring on reserved SMs only
+    {"HP_CRIT_SMS": "74", "HP_CRIT_MODE": "0"},  # reserved SMs' lead warps also serve bulk
+    {"HP_CRIT_SMS": "74", "HP_CRIT_MODE": "2"},  # reserved SMs: critical items only
     {"HP_CRIT_SMS": "148", "HP_R1_THR": "0"},    # every SM reserved; ring 1 on every warp
     {"HP_R1_THR": "100000"},                     # ring 1 on lead warps only
 ]
