@@ -495,6 +495,12 @@ __device__ void trace_cycles(const Bufs& b, int ev, int li, int P, int M, unsign
 #define HP_UNROLL_CORE 2  // tuning: level-pair unroll of the K != 4 core loops
 #endif
 constexpr int kUnrollCore = HP_UNROLL_CORE;
+#ifndef HP_UNROLL_K4
+#define HP_UNROLL_K4 4  // tuning: level-pair unroll of the K = 4 (latency) core loop
+// (lone P = 96 climbs, C3:96: 1 -> 89.2 ms, 2 -> 81.0, 4 -> 77.3, 8 -> 75.6,
+// 12/16 -> 74.8; the C3 sweep is ~1 % slower from 8 up: kept at 4)
+#endif
+constexpr int kUnrollK4 = HP_UNROLL_K4;
 #ifndef HP_ABORT_PAIRS
 #define HP_ABORT_PAIRS 4096  // tuning (C3, 1 GPU: 64 -> 236-249 ms, 128 -> 226-234, 512 -> 218-226, 4096 -> 215-219)
 #endif
@@ -798,7 +804,7 @@ __device__ __forceinline__ void eval_item_fast(const Bufs& b, const Work& w, con
           // unrolled so the scheduler can overlap the tail of one level pair
           // with the next (deeper for K = 4, the latency evaluator)
           if constexpr (K == 4) {
-#pragma unroll 4
+#pragma unroll kUnrollK4
             for (; t <= stop; t += 2) {
               level(I0{}, PF{}, M2{}, t);
               level(I1{}, PF{}, M2{}, t + 1);
@@ -1201,6 +1207,17 @@ __device__ void lb_scan_warp(const Leaf& lf, StageLB* s, int lane) {
   }
 }
 
+// HP_DEBUG_PHASES: cycles per phase of the step logic, summed over every
+// step of the search (lane 0's clock; printed by search_full)
+__device__ unsigned long long g_phase[16];
+#define PHASE_MARK(k)                                                        \
+  if (c_dbg_phases && lane == 0) {                                           \
+    const long long now_ = clock64();                                        \
+    atomicAdd(&g_phase[k], (unsigned long long)(now_ - ph_t));               \
+    ph_t = now_;                                                             \
+  }
+__constant__ int c_dbg_phases;
+
 // Whole warp: screens the neighbours of leaf li's current split (nb_screen;
 // off while the search log is recorded) and lists the survivors in nb_ids.
 // Screened slots get their T_SKIP / T_MEMORY / T_INVALID value in nb right
@@ -1217,6 +1234,7 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
   StageLB* sl = b.lbs + lf.split_off;
   StageNb* sn = b.lbn + lf.split_off;
   const bool screen = b.log.vals == nullptr;
+  long long ph_t = c_dbg_phases ? clock64() : 0;
   const double cur_t = __ldcg(&b.hs[li].cur_time);
   if (screen) {
     // (cur was last written by whichever SM ran the previous step)
@@ -1250,8 +1268,10 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
       }
     }
     __syncwarp();
+    PHASE_MARK(0);
     lb_scan_warp(lf, sl, lane);
     __syncwarp();
+    PHASE_MARK(1);
   }
   // all of the lane's slots first (independent loads in flight together),
   // then the survivor list in slot order
@@ -1269,6 +1289,7 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
     }
   }
   nskip = __reduce_add_sync(0xffffffffu, (unsigned)nskip);
+  PHASE_MARK(2);
   if (lane == 0 && nskip && b.ops) atomicAdd(b.ops + 3, (unsigned long long)nskip);
   int n = 0;
   for (int j = 0; 32 * j < nslots; ++j) {
@@ -1279,6 +1300,7 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
   }
   __threadfence();
   __syncwarp();
+  PHASE_MARK(3);
   return n;
 }
 
@@ -1294,6 +1316,7 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
   int* best = b.best + lf.split_off;
   short* hist = b.hist + b.hist_off[li];
   const double* nb = b.nb + b.nb_off[li];
+  long long ph_t = c_dbg_phases ? clock64() : 0;
   HillState hs;
   hs.cur_time = __ldcg(&b.hs[li].cur_time);
   hs.best_time = __ldcg(&b.hs[li].best_time);
@@ -1457,6 +1480,7 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
     }
   }
 
+  PHASE_MARK(4);
   // ---- neighbour loop: counts, move argmin (time, slot), best candidate
   long long sim = 0, pru = 0;
   double mt = __builtin_huge_val();
@@ -1654,8 +1678,11 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
     }
     if (lane == 0) __stcg(memo + hs.steps, 1);
   }
+  PHASE_MARK(5);
   __threadfence();
   __syncwarp();
+  PHASE_MARK(6);
+  if (c_dbg_phases && lane == 0) atomicAdd(&g_phase[7], 1ULL);
   return active;
 }
 
@@ -1874,6 +1901,7 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
   for (;;) {
     int quit = 0, cls = 0;
     Work w{};
+    long long ph_t = c_dbg_phases ? clock64() : 0;
     if (lane == 0) {
       // priority items go to one warp per SM sub-partition (warps 0-3 of
       // the SM's one block), so two of them never share one: a climb step
@@ -1887,6 +1915,7 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
     }
     quit = __shfl_sync(0xffffffffu, quit, 0);
     if (quit) return;
+    PHASE_MARK(8);
     cls = __shfl_sync(0xffffffffu, cls, 0);
     w.leaf = __shfl_sync(0xffffffffu, w.leaf, 0);
     w.kind = __shfl_sync(0xffffffffu, w.kind, 0);
@@ -1914,6 +1943,7 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
 #endif
     }
     __syncwarp();
+    PHASE_MARK(9);
     if (tr_item && lane == 0) trace_event(b, 2, w.leaf, b.leaves[w.leaf], w.first);
     int last = 0;
     if (lane == 0) {
@@ -1923,6 +1953,8 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
       atomicAdd(q.progress, 1ULL);
     }
     last = __shfl_sync(0xffffffffu, last, 0);
+    PHASE_MARK(10);
+    if (c_dbg_phases && lane == 0) atomicAdd(&g_phase[11], 1ULL);
     if (last) advance_leaf(b, q, w.leaf, lane, true);
     __syncwarp();
   }
@@ -2963,7 +2995,23 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
     const hpk::StagedTables tt = staged(bh, std::getenv("HP_NO_STAGE") ? 0 : 160 * 1024);  // (knob: A/B)
     const size_t dsm = tt.lg_bytes + tt.hop_bytes;
     CK(cudaFuncSetAttribute(hpk::k_hill_async, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    const bool dbg_ph = std::getenv("HP_DEBUG_PHASES") != nullptr;  // diagnostics
+    if (dbg_ph) {
+      static const int on = 1;
+      static const unsigned long long z[16] = {};
+      CK(cudaMemcpyToSymbolAsync(hpk::c_dbg_phases, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyToSymbolAsync(hpk::g_phase, z, sizeof z, 0, cudaMemcpyHostToDevice, st));
+    }
     hpk::k_hill_async<<<grid, threads, dsm, st>>>(bh, q, tt);
+    if (dbg_ph) {
+      unsigned long long ph[16];
+      CK(cudaMemcpyFromSymbolAsync(ph, hpk::g_phase, sizeof ph, 0, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::fprintf(stderr, "HP_DEBUG_PHASES Mcycles: screen rows %.1f scan %.1f slots %.1f list %.1f | "
+                   "step loads+memo %.1f rest %.1f fence %.1f | steps %llu | items %llu: pop %.1f eval %.1f done %.1f\n",
+                   ph[0] / 1e6, ph[1] / 1e6, ph[2] / 1e6, ph[3] / 1e6, ph[4] / 1e6, ph[5] / 1e6, ph[6] / 1e6,
+                   ph[7], ph[11], ph[8] / 1e6, ph[9] / 1e6, ph[10] / 1e6);
+    }
     if (h1) CK(cudaEventRecord(h1, st));
     out.launches += 2;
     out.eval_launches++;
