@@ -1273,31 +1273,41 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
     __syncwarp();
     PHASE_MARK(1);
   }
-  // all of the lane's slots first (independent loads in flight together),
-  // then the survivor list in slot order
-  constexpr int NQ = (2 * HP_MAX_STAGES + 31) / 32;
-  unsigned sv = 0;
+  // One boundary per lane and round (bb = lane + 32 j): both of its slots
+  // read the same rows, loaded as one batch (nb_rows_load) before the two
+  // bounds are computed; the survivors are listed in slot order.
+  int n = 0;
   int nskip = 0;
-#pragma unroll
-  for (int j = 0; j < NQ; ++j) {
-    const int qq = 32 * j + lane;
-    if (qq < nslots) {
-      const double scr = screen ? nb_screen_pre(lf, sl, sn, qq, cur_t) : 0.0;
-      if (scr == 0.0) sv |= 1u << j;
-      else nbt[qq] = scr;
-      nskip += scr == T_SKIP ? 1 : 0;
+  if (screen) {
+#pragma unroll 1
+    for (int j = 0; 32 * j < P - 1; ++j) {
+      const int bb = lane + 32 * j;
+      bool s0 = false, s1 = false;
+      if (bb < P - 1) {
+        NbRows r;
+        nb_rows_load(lf, sl, sn, bb, r);
+        const double c0 = screen_of(nb_lb_rows(lf, r, bb, 0), cur_t);
+        const double c1 = screen_of(nb_lb_rows(lf, r, bb, 1), cur_t);
+        s0 = c0 == 0.0;
+        s1 = c1 == 0.0;
+        if (!s0) nbt[2 * bb] = c0;
+        if (!s1) nbt[2 * bb + 1] = c1;
+        nskip += (c0 == T_SKIP ? 1 : 0) + (c1 == T_SKIP ? 1 : 0);
+      }
+      const unsigned m0 = __ballot_sync(0xffffffffu, s0), m1 = __ballot_sync(0xffffffffu, s1);
+      const unsigned lower = (1u << lane) - 1u;
+      int pos = n + __popc(m0 & lower) + __popc(m1 & lower);
+      if (s0) ids[pos++] = 2 * bb;
+      if (s1) ids[pos] = 2 * bb + 1;
+      n += __popc(m0) + __popc(m1);
     }
+  } else {
+    for (int qq = lane; qq < nslots; qq += 32) ids[qq] = qq;
+    n = nslots;
   }
   nskip = __reduce_add_sync(0xffffffffu, (unsigned)nskip);
   PHASE_MARK(2);
   if (lane == 0 && nskip && b.ops) atomicAdd(b.ops + 3, (unsigned long long)nskip);
-  int n = 0;
-  for (int j = 0; 32 * j < nslots; ++j) {
-    const bool surv = (sv >> j) & 1u;
-    const unsigned m = __ballot_sync(0xffffffffu, surv);
-    if (surv) ids[n + __popc(m & ((1u << lane) - 1u))] = 32 * j + lane;
-    n += __popc(m);
-  }
   __threadfence();
   __syncwarp();
   PHASE_MARK(3);

@@ -249,6 +249,15 @@ struct StageLB {
   double SG, SGY;        // max_{j>=k} GX_j, max_{j>=k} GY_j
 };
 
+// Durations of stage i of the current split at counts cur-1 ([0]) and
+// cur+1 ([1]), the only counts a neighbour gives a stage, with their status:
+// 0 count < 1 (planner.cpp:478), 1 memory-pruned, 2 feasible. Lets the
+// screen (nb_screen_pre) and the neighbour evaluation skip stage_setup.
+struct StageNb {
+  double f[2], b[2], dps[2];
+  int st[2];
+};
+
 HPD double neg_inf() { return -__builtin_huge_val(); }
 
 // Pair-circuit term of the 1F1B bound. On stage k the op after B(k, m) is
@@ -352,44 +361,112 @@ HPD double lb_total(const Leaf& lf, const StageLB* s) {
 // contain a changed stage explicitly, the others through the prefix /
 // suffix maxima shifted by the changed sums (T0 by dA + dB, Bt_{k+1} by dB
 // for k > bb).
-HPD double pair_lb_nb(const Leaf& lf, const StageLB* s, int bb, double f0, double b0, double p0,
-                      double f1, double b1, double p1, double dps0, double dA, double dB) {
+// The current split's row values the bounds of boundary bb's two
+// neighbours read (stages bb-1 .. bb+2 of StageLB, stages bb, bb+1 of
+// StageNb). nb_rows_load reads every one of them unconditionally (indices
+// clamped; the unused ones are ignored), so the device issues them as one
+// batch of independent loads.
+struct NbRows {
+  double nf[2][2], nbw[2][2], nd[2][2];  // [stage bb, bb+1][count -1, +1]
+  int st[2][2];
+  double PX, PY, A, Bt, sf, f, b;        // stage bb
+  double f1, b1, sf1;                    // stage bb+1
+  double SX2, SY2, SG2, SGY2, f2, b2, Bt2, d2;  // stage bb+2 (bb + 2 < P)
+  double PGm, PGYm, fm, bm, sfm;         // stage bb-1 (bb >= 1)
+  double dps0, T0;                       // stage 0's DP sync, lb_total
+};
+
+// (StageLB part)
+HPD void lb_rows_load(const Leaf& lf, const StageLB* s, int bb, NbRows& r) {
+  const int P = lf.P;
+  const int b2 = bb + 2 < P ? bb + 2 : bb + 1, bm = bb >= 1 ? bb - 1 : bb;
+  r.PX = HP_LDX(&s[bb].PX);
+  r.PY = HP_LDX(&s[bb].PY);
+  r.A = HP_LDX(&s[bb].A);
+  r.Bt = HP_LDX(&s[bb].Bt);
+  r.sf = HP_LDX(&s[bb].sf);
+  r.f = HP_LDX(&s[bb].f);
+  r.b = HP_LDX(&s[bb].b);
+  r.f1 = HP_LDX(&s[bb + 1].f);
+  r.b1 = HP_LDX(&s[bb + 1].b);
+  r.sf1 = HP_LDX(&s[bb + 1].sf);
+  r.SX2 = HP_LDX(&s[b2].SX);
+  r.SY2 = HP_LDX(&s[b2].SY);
+  r.SG2 = HP_LDX(&s[b2].SG);
+  r.SGY2 = HP_LDX(&s[b2].SGY);
+  r.f2 = HP_LDX(&s[b2].f);
+  r.b2 = HP_LDX(&s[b2].b);
+  r.Bt2 = HP_LDX(&s[b2].Bt);
+  r.d2 = HP_LDX(&s[b2].dps);
+  r.PGm = HP_LDX(&s[bm].PG);
+  r.PGYm = HP_LDX(&s[bm].PGY);
+  r.fm = HP_LDX(&s[bm].f);
+  r.bm = HP_LDX(&s[bm].b);
+  r.sfm = HP_LDX(&s[bm].sf);
+  r.dps0 = HP_LDX(&s[0].dps);
+  r.T0 = lb_total(lf, s);
+}
+
+HPD void nb_rows_load(const Leaf& lf, const StageLB* s, const StageNb* nbs, int bb, NbRows& r) {
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      r.nf[u][k] = HP_LDX(&nbs[bb + u].f[k]);
+      r.nbw[u][k] = HP_LDX(&nbs[bb + u].b[k]);
+      r.nd[u][k] = HP_LDX(&nbs[bb + u].dps[k]);
+      r.st[u][k] = HP_LDX(&nbs[bb + u].st[k]);
+    }
+  lb_rows_load(lf, s, bb, r);
+}
+
+// Pair-circuit part of the bound of the neighbour that gives stages bb and
+// bb+1 the durations (f0, b0, p0) and (f1, b1, p1): the three pairs that
+// contain a changed stage explicitly, the others through the prefix /
+// suffix maxima shifted by the changed sums (T0 by dA + dB, Bt_{k+1} by dB
+// for k > bb).
+HPD double pair_lb_rows(const Leaf& lf, const NbRows& r, int bb, double f0, double b0, double p0,
+                        double f1, double b1, double p1, double dps0, double dA, double dB) {
 #ifdef HP_NO_PAIR_LB
   return neg_inf();  // tuning / A-B: per-stage bound only
 #endif
   if (lf.sched != 1) return neg_inf();
   const int P = lf.P;
   const long long M = lf.M;
-  const double T = lb_total(lf, s) + (dA + dB);
+  const double T = r.T0 + (dA + dB);
   double g = neg_inf(), gy = neg_inf();
   if (bb >= 1) {
-    g = HP_LDX(&s[bb - 1].PG);
-    gy = HP_LDX(&s[bb - 1].PGY);
+    g = r.PGm;
+    gy = r.PGYm;
     // pair (bb-1, bb)
-    const double fk = HP_LDX(&s[bb - 1].f), bk = HP_LDX(&s[bb - 1].b), sfk = HP_LDX(&s[bb - 1].sf);
-    const double G = pair_gain(M, P, bb - 1, pair_cyc(fk, bk, f0, b0, sfk), b0);
+    const double G = pair_gain(M, P, bb - 1, pair_cyc(r.fm, r.bm, f0, b0, r.sfm), b0);
     g = dmax(g, G);
-    gy = dmax(gy, G - HP_LDX(&s[bb].Bt) + p0);
+    gy = dmax(gy, G - r.Bt + p0);
   }
-  const double sfb = HP_LDX(&s[bb].sf);
-  const double Bt1 = HP_LDX(&s[bb].Bt) + sfb + b0;  // the neighbour's Bt_{bb+1}
+  const double Bt1 = r.Bt + r.sf + b0;  // the neighbour's Bt_{bb+1}
   {
     // pair (bb, bb+1)
-    const double G = pair_gain(M, P, bb, pair_cyc(f0, b0, f1, b1, sfb), b1);
+    const double G = pair_gain(M, P, bb, pair_cyc(f0, b0, f1, b1, r.sf), b1);
     g = dmax(g, G);
     gy = dmax(gy, G - Bt1 + p1);
   }
   if (bb + 2 < P) {
     // pair (bb+1, bb+2)
-    const double fe = HP_LDX(&s[bb + 2].f), be = HP_LDX(&s[bb + 2].b);
-    const double G = pair_gain(M, P, bb + 1, pair_cyc(f1, b1, fe, be, HP_LDX(&s[bb + 1].sf)), be);
+    const double G = pair_gain(M, P, bb + 1, pair_cyc(f1, b1, r.f2, r.b2, r.sf1), r.b2);
     g = dmax(g, G);
-    gy = dmax(gy, G - (HP_LDX(&s[bb + 2].Bt) + dB) + HP_LDX(&s[bb + 2].dps));
+    gy = dmax(gy, G - (r.Bt2 + dB) + r.d2);
     // pairs bb+2 .. P-2
-    g = dmax(g, HP_LDX(&s[bb + 2].SG));
-    gy = dmax(gy, HP_LDX(&s[bb + 2].SGY) - dB);
+    g = dmax(g, r.SG2);
+    gy = dmax(gy, r.SGY2 - dB);
   }
   return dmax(T + g + dps0, T + gy);
+}
+
+HPD double pair_lb_nb(const Leaf& lf, const StageLB* s, int bb, double f0, double b0, double p0,
+                      double f1, double b1, double p1, double dps0, double dA, double dB) {
+  NbRows r;
+  lb_rows_load(lf, s, bb, r);
+  return pair_lb_rows(lf, r, bb, f0, b0, p0, f1, b1, p1, dps0, dA, dB);
 }
 
 // Screens neighbour slot q of `cur` (boundary q >> 1, +1 for even q):
@@ -427,15 +504,6 @@ HPD double nb_screen(const Consts& c, const Leaf& lf, const LeafGroup* lg, const
   return lb > cur_t * (1.0 + kScreenMargin) ? T_SKIP : 0.0;
 }
 
-// Durations of stage i of the current split at counts cur-1 ([0]) and
-// cur+1 ([1]), the only counts a neighbour gives a stage, with their status:
-// 0 count < 1 (planner.cpp:478), 1 memory-pruned, 2 feasible. Lets the
-// screen (nb_screen_pre) and the neighbour evaluation skip stage_setup.
-struct StageNb {
-  double f[2], b[2], dps[2];
-  int st[2];
-};
-
 HPD void lb_stage_nb(const Consts& c, const Leaf& lf, const LeafGroup* lg, const uint8_t* slots,
                      const double* hop, int i, int count, StageNb& n) {
 #pragma unroll
@@ -452,34 +520,37 @@ HPD void lb_stage_nb(const Consts& c, const Leaf& lf, const LeafGroup* lg, const
   }
 }
 
-// nb_screen's path lower bound of neighbour slot q with the changed stages'
-// durations taken from StageNb rows (same value for every slot). Returns
-// T_INVALID / T_MEMORY for an infeasible neighbour, else the bound (>= 0).
-HPD double nb_lb_pre(const Leaf& lf, const StageLB* s, const StageNb* nbs, int q) {
+// nb_screen's path lower bound of neighbour slot q = 2 bb + odd with the
+// changed stages' durations taken from the StageNb rows in r (same value for
+// every slot). Returns T_INVALID / T_MEMORY for an infeasible neighbour,
+// else the bound (>= 0).
+HPD double nb_lb_rows(const Leaf& lf, const NbRows& r, int bb, int odd) {
   const int P = lf.P;
-  const int bb = q >> 1;
-  const int k0 = (q & 1) ? 0 : 1;  // +1 moves a layer into stage bb, out of bb+1
+  const int k0 = odd ? 0 : 1;  // +1 moves a layer into stage bb, out of bb+1
   const int k1 = 1 - k0;
-  const int st0 = HP_LDX(&nbs[bb].st[k0]), st1 = HP_LDX(&nbs[bb + 1].st[k1]);
+  const int st0 = r.st[0][k0], st1 = r.st[1][k1];
   if (st0 == 0 || st1 == 0) return T_INVALID;
   if (st0 == 1 || st1 == 1) return T_MEMORY;
-  const double f0 = HP_LDX(&nbs[bb].f[k0]), b0 = HP_LDX(&nbs[bb].b[k0]), p0 = HP_LDX(&nbs[bb].dps[k0]);
-  const double f1 = HP_LDX(&nbs[bb + 1].f[k1]), b1 = HP_LDX(&nbs[bb + 1].b[k1]);
-  const double p1 = HP_LDX(&nbs[bb + 1].dps[k1]);
+  const double f0 = r.nf[0][k0], b0 = r.nbw[0][k0], p0 = r.nd[0][k0];
+  const double f1 = r.nf[1][k1], b1 = r.nbw[1][k1], p1 = r.nd[1][k1];
   const double M = (double)lf.M;
-  const double dps0 = bb == 0 ? p0 : HP_LDX(&s[0].dps);
-  double lb = dmax(HP_LDX(&s[bb].PX) + dps0, HP_LDX(&s[bb].PY));
-  const double A0 = HP_LDX(&s[bb].A), B0 = HP_LDX(&s[bb].Bt), sf0 = HP_LDX(&s[bb].sf);
+  const double dps0 = bb == 0 ? p0 : r.dps0;
+  double lb = dmax(r.PX + dps0, r.PY);
+  const double A0 = r.A, B0 = r.Bt, sf0 = r.sf;
   lb = dmax(lb, A0 + M * (f0 + b0) + dmax(B0 + dps0, p0));
   const double A1 = A0 + f0 + sf0, B1 = B0 + sf0 + b0;
   lb = dmax(lb, A1 + M * (f1 + b1) + dmax(B1 + dps0, p1));
-  const double fbb = HP_LDX(&s[bb].f), fb1 = HP_LDX(&s[bb + 1].f);
-  const double bbb = HP_LDX(&s[bb].b), bb1 = HP_LDX(&s[bb + 1].b);
-  const double dA = (f0 - fbb) + (f1 - fb1);
-  const double dB = (b0 - bbb) + (b1 - bb1);
-  if (bb + 2 < P) lb = dmax(lb, dmax(HP_LDX(&s[bb + 2].SX) + dA + dB + dps0, HP_LDX(&s[bb + 2].SY) + dA));
-  lb = dmax(lb, pair_lb_nb(lf, s, bb, f0, b0, p0, f1, b1, p1, dps0, dA, dB));
+  const double dA = (f0 - r.f) + (f1 - r.f1);
+  const double dB = (b0 - r.b) + (b1 - r.b1);
+  if (bb + 2 < P) lb = dmax(lb, dmax(r.SX2 + dA + dB + dps0, r.SY2 + dA));
+  lb = dmax(lb, pair_lb_rows(lf, r, bb, f0, b0, p0, f1, b1, p1, dps0, dA, dB));
   return dmax(lb, 0.0);
+}
+
+HPD double nb_lb_pre(const Leaf& lf, const StageLB* s, const StageNb* nbs, int q) {
+  NbRows r;
+  nb_rows_load(lf, s, nbs, q >> 1, r);
+  return nb_lb_rows(lf, r, q >> 1, q & 1);
 }
 
 // Screen decision from nb_lb_pre: T_INVALID / T_MEMORY, T_SKIP when the
