@@ -1350,9 +1350,18 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
       nv[k][1] = __ldcg(nb + 2 * bb + 1);
     }
   }
-  int cv[8];  // cur[i0 + r] (C <= 8)
+  int cv[8], rv2[2][8];  // cur[i0 + r] (C <= 8); the seeds' (uniform, proportional)
+  {
+    const int* ru = b.uni + lf.split_off;
+    const int* rp = b.prop + lf.split_off;
 #pragma unroll
-  for (int r = 0; r < 8; ++r) cv[r] = i0 + r < i1 ? __ldcg(cur + i0 + r) : 0;
+    for (int r = 0; r < 8; ++r) {
+      const bool in = i0 + r < i1;
+      cv[r] = in ? __ldcg(cur + i0 + r) : 0;
+      rv2[0][r] = in ? ru[i0 + r] : 0;
+      rv2[1][r] = in ? rp[i0 + r] : 0;
+    }
+  }
   long long g_sim = 0, g_pru = 0;
   if (lane == 0) {
     g_sim = __ldcg(&b.hs[li].simulated);
@@ -1451,11 +1460,9 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
   }
   // seeds at distance 1: prefix sums of cur - ref over each lane's chunk
   {
-    for (int sd = 0; sd < 2; ++sd) {
-      const int* ref = (sd == 0 ? b.uni : b.prop) + lf.split_off;
-      int rv[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) rv[r] = i0 + r < i1 ? ref[i0 + r] : 0;
+    for (int sd = 0; sd < 2; ++sd) {
+      const int (&rv)[8] = rv2[sd];
       int loc = 0;
 #pragma unroll
       for (int r = 0; r < 8; ++r) loc += cv[r] - rv[r];
@@ -1650,10 +1657,12 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
       if (top - 32 * v < 0) break;
       const int idx = top - 32 * v - lane;
       int x = (idx >= 0 && (hv[v] >> 1) == mb) ? ((hv[v] & 1) ? -1 : 1) : 0;
+      if (__ballot_sync(FULL, x != 0)) {  // (most blocks hold no move of boundary mb)
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, x, o);
-        if (lane >= o) x += y;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, x, o);
+          if (lane >= o) x += y;
+        }
       }
       const int c = carry + x;
       if (idx >= 0) __stcg(memo + idx, dv[v] + abs(c + md) - abs(c));
