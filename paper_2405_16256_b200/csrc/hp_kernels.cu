@@ -1120,8 +1120,7 @@ __device__ void lb_scan_warp(const Leaf& lf, StageLB* s, int lane) {
   for (int r = 0; r < 8; ++r) {
     const int i = i0 + r;
     if (i < i1) {
-      __stcg(&s[i].A, A);
-      __stcg(&s[i].Bt, Bt);
+      __stcg(reinterpret_cast<double2*>(&s[i].A), make_double2(A, Bt));
       const double core = A + M * (f[r] + bk[r]);
       X[r] = core + Bt;
       Y[r] = core + dps[r];
@@ -1137,8 +1136,7 @@ __device__ void lb_scan_warp(const Leaf& lf, StageLB* s, int lane) {
   for (int r = 0; r < 8; ++r) {
     const int i = i0 + r;
     if (i < i1) {
-      __stcg(&s[i].PX, px);
-      __stcg(&s[i].PY, py);
+      __stcg(reinterpret_cast<double2*>(&s[i].PX), make_double2(px, py));
       px = dmax(px, X[r]);
       py = dmax(py, Y[r]);
     }
@@ -1150,8 +1148,7 @@ __device__ void lb_scan_warp(const Leaf& lf, StageLB* s, int lane) {
     if (i < i1) {
       sx = dmax(sx, X[r]);
       sy = dmax(sy, Y[r]);
-      __stcg(&s[i].SX, sx);
-      __stcg(&s[i].SY, sy);
+      __stcg(reinterpret_cast<double2*>(&s[i].SX), make_double2(sx, sy));
     }
   }
   // pair circuits (pair_gain, lb_scan): pair i needs stage i+1's f, b, dps
@@ -1189,8 +1186,7 @@ __device__ void lb_scan_warp(const Leaf& lf, StageLB* s, int lane) {
   for (int r = 0; r < 8; ++r) {
     const int i = i0 + r;
     if (i < i1) {
-      __stcg(&s[i].PG, pg);
-      __stcg(&s[i].PGY, pgy);
+      __stcg(reinterpret_cast<double2*>(&s[i].PG), make_double2(pg, pgy));
       pg = dmax(pg, gx[r]);
       pgy = dmax(pgy, gy[r]);
     }
@@ -1201,22 +1197,35 @@ __device__ void lb_scan_warp(const Leaf& lf, StageLB* s, int lane) {
     if (i < i1) {
       sg = dmax(sg, gx[r]);
       sgy = dmax(sgy, gy[r]);
-      __stcg(&s[i].SG, sg);
-      __stcg(&s[i].SGY, sgy);
+      __stcg(reinterpret_cast<double2*>(&s[i].SG), make_double2(sg, sgy));
     }
   }
 }
 
 // HP_DEBUG_PHASES: cycles per phase of the step logic, summed over every
 // step of the search (lane 0's clock; printed by search_full)
+// Compiled in only with -DHP_PHASES=1 (tools/tune/build_variants.py): even
+// untaken, the checks in the item loop cost the C3 sweep ~7 %.
+#ifndef HP_PHASES
+#define HP_PHASES 0
+#endif
 __device__ unsigned long long g_phase[16];
+__constant__ int c_dbg_phases;
+#if HP_PHASES
+#define PHASE_T0 long long ph_t = c_dbg_phases ? clock64() : 0
 #define PHASE_MARK(k)                                                        \
   if (c_dbg_phases && lane == 0) {                                           \
     const long long now_ = clock64();                                        \
     atomicAdd(&g_phase[k], (unsigned long long)(now_ - ph_t));               \
     ph_t = now_;                                                             \
   }
-__constant__ int c_dbg_phases;
+#define PHASE_COUNT(k) \
+  if (c_dbg_phases && lane == 0) atomicAdd(&g_phase[k], 1ULL)
+#else
+#define PHASE_T0 (void)0
+#define PHASE_MARK(k) (void)0
+#define PHASE_COUNT(k) (void)0
+#endif
 
 // Whole warp: screens the neighbours of leaf li's current split (nb_screen;
 // off while the search log is recorded) and lists the survivors in nb_ids.
@@ -1234,7 +1243,7 @@ __device__ int screen_neighbours(const Bufs& b, int li, const Leaf& lf, int lane
   StageLB* sl = b.lbs + lf.split_off;
   StageNb* sn = b.lbn + lf.split_off;
   const bool screen = b.log.vals == nullptr;
-  long long ph_t = c_dbg_phases ? clock64() : 0;
+  PHASE_T0;
   const double cur_t = __ldcg(&b.hs[li].cur_time);
   if (screen) {
     // (cur was last written by whichever SM ran the previous step)
@@ -1326,7 +1335,7 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
   int* best = b.best + lf.split_off;
   short* hist = b.hist + b.hist_off[li];
   const double* nb = b.nb + b.nb_off[li];
-  long long ph_t = c_dbg_phases ? clock64() : 0;
+  PHASE_T0;
   HillState hs;
   hs.cur_time = __ldcg(&b.hs[li].cur_time);
   hs.best_time = __ldcg(&b.hs[li].best_time);
@@ -1701,7 +1710,7 @@ __device__ int hill_step_warp(const Bufs& b, int li, const Leaf& lf, int lane, i
   __threadfence();
   __syncwarp();
   PHASE_MARK(6);
-  if (c_dbg_phases && lane == 0) atomicAdd(&g_phase[7], 1ULL);
+  PHASE_COUNT(7);
   return active;
 }
 
@@ -1920,7 +1929,7 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
   for (;;) {
     int quit = 0, cls = 0;
     Work w{};
-    long long ph_t = c_dbg_phases ? clock64() : 0;
+    PHASE_T0;
     if (lane == 0) {
       // priority items go to one warp per SM sub-partition (warps 0-3 of
       // the SM's one block), so two of them never share one: a climb step
@@ -1973,7 +1982,7 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     PHASE_MARK(10);
-    if (c_dbg_phases && lane == 0) atomicAdd(&g_phase[11], 1ULL);
+    PHASE_COUNT(11);
     if (last) advance_leaf(b, q, w.leaf, lane, true);
     __syncwarp();
   }

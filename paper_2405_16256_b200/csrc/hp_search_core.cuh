@@ -3,6 +3,8 @@
 // (tests/emu). Pure functions of their arguments; no CUDA intrinsics.
 #pragma once
 
+#include <cstddef>
+
 #include "hp_core.cuh"
 
 namespace hpc {
@@ -248,6 +250,12 @@ struct StageLB {
   double PG, PGY;        // max_{j<k} GX_j, max_{j<k} GY_j (pair circuits, pair_gain)
   double SG, SGY;        // max_{j>=k} GX_j, max_{j>=k} GY_j
 };
+// (the device writes the pairs A/Bt, PX/PY, SX/SY, PG/PGY, SG/SGY as one
+// 16-byte store each)
+static_assert(sizeof(StageLB) % 16 == 0 && offsetof(StageLB, A) % 16 == 0 && offsetof(StageLB, PX) % 16 == 0 &&
+                  offsetof(StageLB, SX) % 16 == 0 && offsetof(StageLB, PG) % 16 == 0 &&
+                  offsetof(StageLB, SG) % 16 == 0,
+              "StageLB pair layout");
 
 // Durations of stage i of the current split at counts cur-1 ([0]) and
 // cur+1 ([1]), the only counts a neighbour gives a stage, with their status:
