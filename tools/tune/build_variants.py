@@ -1,8 +1,9 @@
 """Builds tuning variants of the product library (compile-time -D knobs)
-into tools/tune/_lib/<name>.so for A/B timing on the GPU:
+into tools/tune/ab/<name>.so (git-ignored, travels with gpurun) for A/B
+timing on the GPU (tools/gpu/lib_ab.sh, tools/gpu/bench_lib_ab.sh):
 
     python tools/tune/build_variants.py name1=DEF1,DEF2 name2=...
-    HP_LIB=tools/tune/_lib/name1.so python tools/run_search.py C3 full 3
+    HP_LIB=tools/tune/ab/name1.so python tools/run_search.py C3 full 3
 """
 import os
 import sys
@@ -12,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 from paper_2405_16256_b200 import build  # noqa: E402
 
-OUT = os.path.join(ROOT, "tools", "tune", "_lib")
+OUT = os.path.join(ROOT, "tools", "tune", "ab")
 
 
 def one(spec):
