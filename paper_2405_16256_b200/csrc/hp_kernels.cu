@@ -1938,7 +1938,9 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
       int lv0 = wib < 4 || !q.lead ? 0 : 1;
       if (q.crit_sms > 0) lv0 = crit_blk && wib < 4 ? 0 : 1;
       const int lv_end = crit_blk && wib < 4 && q.crit_mode != 0 ? 1 : kRings;
-      quit = pop_item(q, w, tk, lv0, wib < 4, lv_end) ? 0 : 1;
+      // (on a reserved SM in mode 1, warps 4-7 are the SM's ring-1 servers)
+      const bool lead = wib < 4 || (crit_blk && q.crit_mode == 1);
+      quit = pop_item(q, w, tk, lv0, lead, lv_end) ? 0 : 1;
       if (!quit) cls = w.out > 0 ? w.out - 1 : leaf_class(b.leaves[w.leaf]);
     }
     quit = __shfl_sync(0xffffffffu, quit, 0);
@@ -2992,6 +2994,11 @@ hph::Status search_full(Arena& a, const hph::Problem& p, const std::vector<int>&
       // 2 GPUs with the reservation in mode 1: 124.0 -> 123.2, not adopted)
       q.crit_mode = 1;
       if (const char* e = std::getenv("HP_CRIT_MODE")) q.crit_mode = std::atoi(e);  // tuning
+      // rings 1 and 2 need servers: with every SM reserved, warps 4-7 serve
+      // them (mode 2 would leave none), and blocks of <= 4 warps have no
+      // warps 4-7 at all
+      if (q.crit_mode == 2 && q.crit_sms >= grid) q.crit_mode = 1;
+      if (threads <= 128) q.crit_mode = 0;
       long long budget = (long long)(q.crit_sms > 0 ? q.crit_sms : grid) * (q.lead ? 4 : threads / 32);
       if (const char* e = std::getenv("HP_CRIT_WARPS")) budget = std::atoll(e);  // tuning
       std::vector<int> byest(climb);

@@ -91,6 +91,9 @@ SCHED_KNOBS = [
     {"HP_CRIT_SMS": "74", "HP_CRIT_MODE": "0"},  # reserved SMs' lead warps also serve bulk
     {"HP_CRIT_SMS": "74", "HP_CRIT_MODE": "2"},  # reserved SMs: critical items only
     {"HP_CRIT_SMS": "148", "HP_R1_THR": "0"},    # every SM reserved; ring 1 on every warp
+    {"HP_CRIT_SMS": "148"},                      # every SM reserved: warps 4-7 serve rings 1/2
+    {"HP_CRIT_SMS": "148", "HP_CRIT_MODE": "2"},  # (mode 2 falls back to 1: rings 1/2 need servers)
+    {"HP_CRIT_SMS": "74", "HP_ASYNC_THREADS": "128"},  # 4-warp blocks: no ring-0-only warps
     {"HP_R1_THR": "100000"},                     # ring 1 on lead warps only
 ]
 
