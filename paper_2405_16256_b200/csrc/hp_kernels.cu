@@ -1938,8 +1938,10 @@ __global__ void __launch_bounds__(HP_ASYNC_MAXT, HP_ALL_MINB) k_hill_async(Bufs 
       int lv0 = wib < 4 || !q.lead ? 0 : 1;
       if (q.crit_sms > 0) lv0 = crit_blk && wib < 4 ? 0 : 1;
       const int lv_end = crit_blk && wib < 4 && q.crit_mode != 0 ? 1 : kRings;
-      // (on a reserved SM in mode 1, warps 4-7 are the SM's ring-1 servers)
-      const bool lead = wib < 4 || (crit_blk && q.crit_mode == 1);
+      // (with every SM reserved in mode 1, warps 4-7 are the only ring-1
+      // servers; otherwise the unreserved SMs' lead warps are, and warps 4-7
+      // of the reserved ones taking ring 1 eagerly costs 4 GPUs 86 -> 97 ms)
+      const bool lead = wib < 4 || (crit_blk && q.crit_mode == 1 && q.crit_sms >= (int)gridDim.x);
       quit = pop_item(q, w, tk, lv0, lead, lv_end) ? 0 : 1;
       if (!quit) cls = w.out > 0 ? w.out - 1 : leaf_class(b.leaves[w.leaf]);
     }
