@@ -499,16 +499,10 @@ HPD double nb_screen(const Consts& c, const Leaf& lf, const LeafGroup* lg, const
   lb = dmax(lb, A0 + M * (d0.f + d0.b) + dmax(B0 + dps0, d0.dps));
   const double A1 = A0 + d0.f + s[bb].sf, B1 = B0 + s[bb].sf + d0.b;
   lb = dmax(lb, A1 + M * (d1.f + d1.b) + dmax(B1 + dps0, d1.dps));
-  if (bb + 2 < P) {
-    const double dA = (d0.f - s[bb].f) + (d1.f - s[bb + 1].f);
-    const double dB = (d0.b - s[bb].b) + (d1.b - s[bb + 1].b);
-    lb = dmax(lb, dmax(s[bb + 2].SX + dA + dB + dps0, s[bb + 2].SY + dA));
-  }
-  {
-    const double dA = (d0.f - s[bb].f) + (d1.f - s[bb + 1].f);
-    const double dB = (d0.b - s[bb].b) + (d1.b - s[bb + 1].b);
-    lb = dmax(lb, pair_lb_nb(lf, s, bb, d0.f, d0.b, d0.dps, d1.f, d1.b, d1.dps, dps0, dA, dB));
-  }
+  const double dA = (d0.f - s[bb].f) + (d1.f - s[bb + 1].f);
+  const double dB = (d0.b - s[bb].b) + (d1.b - s[bb + 1].b);
+  if (bb + 2 < P) lb = dmax(lb, dmax(s[bb + 2].SX + dA + dB + dps0, s[bb + 2].SY + dA));
+  lb = dmax(lb, pair_lb_nb(lf, s, bb, d0.f, d0.b, d0.dps, d1.f, d1.b, d1.dps, dps0, dA, dB));
   return lb > cur_t * (1.0 + kScreenMargin) ? T_SKIP : 0.0;
 }
 
